@@ -1,0 +1,190 @@
+"""Pin the CPU oracle against golden vectors produced by the live reference
+(``oracle/gen_golden.py``).  CPU only."""
+
+import numpy as np
+import pytest
+
+from oracle import attention as OA
+from oracle import placement as OP
+from oracle import recovery as OR
+from oracle import routing as ORT
+
+
+def _ikeys(d):
+    return {int(k): v for k, v in d.items()}
+
+
+def test_placement_tables(golden):
+    g = golden("placement")
+    assert len(g["cases"]) >= 100
+    for c in g["cases"]:
+        assert OP.owner_table(c["mode"], c["L"], c["H"], c["alive"]) == c["owner"], c
+        assert OP.shard_owner_table(c["num_shards"], c["alive"]) == c["shard_owner"]
+
+
+def test_on_demand_chains(golden):
+    for chain in golden("placement")["chains"]:
+        owner, shards = chain["initial"], chain["initial_shards"]
+        alive = list(range(8))
+        for step in chain["steps"]:
+            alive = [x for x in alive if x != step["fail"]]
+            owner, shards = OP.on_demand_target(owner, shards, alive)
+            assert owner == step["owner"]
+            assert shards == step["shard_owner"]
+
+
+def test_llama70b_chain_shapes(golden):
+    """hybrid(8) -> 7 -> 6 -> 5 gives 1 TP head per survivor and
+    1/2/3 replicated heads per layer; shards 32 -> 38/37 -> 45/44."""
+    chain = [c for c in golden("placement")["chains"] if c["mode"] == "hybrid"][0]
+    for k, step in enumerate(chain["steps"]):
+        for row in step["owner"]:
+            assert row.count(-1) == k + 1
+        counts = {}
+        for o in step["shard_owner"]:
+            counts[o] = counts.get(o, 0) + 1
+        assert max(counts.values()) - min(counts.values()) <= 1
+
+
+def test_footprints(golden):
+    for c in golden("placement")["footprints"]:
+        owner = OP.owner_table(c["mode"], c["L"], c["H"], range(c["n"]))
+        fp = OP.kv_footprint(owner, range(c["n"]), _ikeys(c["tokens"]), _ikeys(c["routing"]),
+                             c["unit"])
+        assert fp == _ikeys(c["footprint"])
+
+
+def test_routing(golden):
+    g = golden("routing")
+    for c in g["cases"]:
+        ranks, load = ORT.route_sequence(c["requests"], range(c["n"]),
+                                         include_decode=c["include_decode"])
+        assert ranks == c["ranks"]
+        assert [load[r] for r in range(c["n"])] == c["workload"]  # bit-exact floats
+    inter = g["interleaved"]
+    router = ORT.Router(range(3))
+    decoded = {}
+    for ev in inter["events"]:
+        kind, rid, rank = ev
+        i, o = inter["requests"][rid]
+        if kind == "route":
+            assert router.route(i, o) == rank
+        else:
+            decoded[rid] = decoded.get(rid, 0) + 1
+            router.decode_token(rank, i, decoded[rid])
+    assert [router.load[r] for r in range(3)] == inter["workload"]
+
+
+def test_weight_recovery(golden):
+    for c in golden("recovery")["weight"]:
+        xf, tgt, tshards = OR.weight_plan(c["wmode"], c["mode"], c["owner"], c["shard_owner"],
+                                          range(c["n"]), c["new_alive"], c["shard_bytes"],
+                                          c["head_bytes"])
+        assert [[d, b, m, k, list(t)] for d, b, m, k, t in xf] == c["transfers"]
+        assert tgt == c["target_owner"]
+        assert tshards == c["target_shards"]
+
+
+def test_kv_recovery(golden):
+    for c in golden("recovery")["kv"]:
+        xf, rt, rs = OR.kv_plan(c["mode"], c["old_owner"], c["new_owner"], c["surv"],
+                                _ikeys(c["contexts"]), _ikeys(c["backed"]),
+                                _ikeys(c["old_routing"]), _ikeys(c["new_routing"]), c["unit"])
+        assert [[d, b, m, k, list(t)] for d, b, m, k, t in xf] == c["transfers"]
+        assert rt == _ikeys(c["recompute_tokens"])
+        assert rs == _ikeys(c["recompute_start"])
+
+
+def test_backup_dynamics(golden):
+    for c in golden("recovery")["backup"]:
+        st = OR.new_backup(c["host"], c["unit"])
+        for step in c["steps"]:
+            for r in step["finish"]:
+                if r in st["backed"] and r not in st["finished"]:
+                    st["finished"].append(r)
+            OR.backup_step(st, step["elapsed"], _ikeys(step["new"]), c["pcie"], c["frac"])
+            assert st["backed"] == _ikeys(step["backed"])
+            assert st["lag"] == _ikeys(step["lag"])
+            assert st["used"] == step["used"]
+            assert st["carry"] == step["carry"]
+            assert st["evictions"] == step["evictions"]
+
+
+def _layers(case):
+    return [{k: np.array(v) for k, v in lw.items()} for lw in case["layers"]]
+
+
+def test_forward_restatement(golden):
+    for c in golden("forward")["cases"]:
+        layers = _layers(c)
+        x = np.array(c["x"])
+        ref = OA.reference_forward(layers, x, c["seq_lens"])
+        np.testing.assert_allclose(ref, np.array(c["reference_out"]), rtol=0, atol=1e-12)
+        par = OA.parallel_forward(layers, c["owner"], c["shard_owner"], range(c["world"]),
+                                  _ikeys(c["routing"]), x, c["seq_lens"])
+        np.testing.assert_allclose(par, np.array(c["parallel_out"]), rtol=0, atol=1e-12)
+
+
+def test_decode_restatement(golden):
+    g = golden("decode")
+    hd = g["head_dim"]
+    for c in g["cases"]:
+        x = np.array(c["x"])
+        start = 0
+        for t, length in enumerate(c["seq_lens"]):
+            seg = x[start:start + length]
+            q = np.stack([seg[-1] * np.array(d) for d in c["diag"]])
+            out = OA.head_decode(q, seg, seg, 1.0 / np.sqrt(hd))
+            np.testing.assert_allclose(out, np.array(c["out"][t]), rtol=0, atol=1e-12)
+            start += length
+
+
+def test_paged_decode_matches_dense():
+    rng = np.random.default_rng(0)
+    hd, ps, qpk = 16, 4, 2
+    lens = [1, 4, 5, 13]
+    n_pages = sum((l + ps - 1) // ps for l in lens) + 3
+    perm = rng.permutation(n_pages)
+    k_pool = rng.standard_normal((n_pages, ps, hd))
+    v_pool = rng.standard_normal((n_pages, ps, hd))
+    bt = np.zeros((len(lens), 8), dtype=np.int64)
+    nxt = 0
+    for s, l in enumerate(lens):
+        for p in range((l + ps - 1) // ps):
+            bt[s, p] = perm[nxt]
+            nxt += 1
+    q = rng.standard_normal((len(lens), qpk, hd))
+    out = OA.paged_decode(q, k_pool, v_pool, bt, range(len(lens)), lens, range(len(lens)),
+                          len(lens), 0.25, ps)
+    for s, l in enumerate(lens):
+        pages = bt[s, :(l + ps - 1) // ps]
+        k = k_pool[pages].reshape(-1, hd)[:l]
+        v = v_pool[pages].reshape(-1, hd)[:l]
+        w = np.exp((q[s] @ k.T) * 0.25)
+        w /= w.sum(1, keepdims=True)
+        np.testing.assert_allclose(out[s], w @ v, atol=1e-12)
+
+
+@pytest.mark.skipif(not __import__("os").path.isdir("/root/reference/pkg/src"),
+                    reason="live reference only present in the build container")
+def test_oracle_against_live_reference_random():
+    """Extra randomized cross-check against the live reference (build
+    container only; the GPU box has no /root/reference)."""
+    import random
+    import sys
+    sys.path.insert(0, "/root/reference/pkg/src")
+    from failsafe.core import ModelSpec
+    from failsafe.placement import make_placement
+    rng = random.Random(5)
+    for _ in range(200):
+        H = rng.randint(1, 20)
+        n = rng.randint(1, min(H, 12))
+        L = rng.randint(1, 30)
+        alive = sorted(rng.sample(range(16), n))
+        m = ModelSpec(num_layers=L, num_kv_heads=H, num_q_heads=H, head_dim=8, hidden_dim=8,
+                      ffn_intermediate_dim=720)
+        for mode in ("naive", "cyclic", "hybrid"):
+            plan = make_placement(mode, m, alive, 16)
+            tab = [[(-1 if a.owner_of(h) is None else a.owner_of(h)) for h in range(H)]
+                   for a in plan.per_layer]
+            assert OP.owner_table(mode, L, H, alive) == tab
