@@ -1,0 +1,174 @@
+/*
+ * failsafe_b200.h -- C ABI of the B200-native FailSafe hybrid-attention
+ * decode hot path (libfailsafe_b200.so).
+ *
+ * Plain C: fixed-width integers, raw pointers, sizes; no torch / CUDA types
+ * in the signatures (streams are passed as `void*` = cudaStream_t).  Every
+ * entry point returns an int status:
+ *
+ *   FS_OK            0
+ *   FS_EVALIDATION   1  -> failsafe.ValidationError  (reference core.py:17-22)
+ *   FS_ESIMULATION   2  -> failsafe.SimulationError  (reference core.py:25-26)
+ *   FS_ECUDA         3  -> CUDA error, surfaced as SimulationError
+ *
+ * with a thread-local message in fs_last_error().  All buffers are caller
+ * owned; nothing allocates on the hot path; no internal threads; results
+ * are deterministic for a fixed device (the stream-K split depends only on
+ * the SM count).
+ *
+ * Reference interfaces replaced (all in /root/reference/pkg/src/failsafe):
+ *   fs_plan_placement   <- placement.make_placement        placement.py:180-186
+ *                          (naive/cyclic _block_plan 117-135, hybrid 148-170)
+ *   fs_plan_ffn         <- placement.ffn_assignment        placement.py:94-114
+ *   fs_plan_on_demand   <- recovery.plan_weight_recovery(.., "on_demand")
+ *                          target placement               recovery.py:323-340, 396-427
+ *   fs_kv_footprint     <- placement.memory_footprint      placement.py:206-236
+ *   fs_plan_pages       <- (new) device page/work table for one decode step;
+ *                          the device form of the per-rank head residency of
+ *                          refexec.ShardedView            refexec.py:136-148
+ *   fs_decode_attention <- the attention half of refexec.parallel_forward
+ *                          (TP heads on owners, DP heads on routed rank)
+ *                                                          refexec.py:281-297, 85-103
+ *   fs_kv_write / fs_kv_read <- (new) KV append into / read from pages
+ *   fs_pages_gather     <- recovery.advance_backup executed as an incremental
+ *                          page copy to pinned host       recovery.py:193-247
+ *   fs_pages_scatter    <- recovery.plan_kv_recovery "pcie_host" kv_slice
+ *                          transfers executed             recovery.py:430-504
+ *   fs_copy_peer        <- recovery.plan_weight_recovery transfers executed
+ *                          peer-to-peer over NVLink       recovery.py:396-427
+ */
+#ifndef FAILSAFE_B200_H
+#define FAILSAFE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FS_OK 0
+#define FS_EVALIDATION 1
+#define FS_ESIMULATION 2
+#define FS_ECUDA 3
+
+#define FS_ABI_VERSION 1
+
+/* owner-table value of a replicated (data-parallel) head */
+#define FS_REPLICATED (-1)
+
+/* placement modes (placement.py:173-177) */
+#define FS_MODE_NAIVE 0
+#define FS_MODE_CYCLIC 1
+#define FS_MODE_HYBRID 2
+
+/* Page format: one page holds FS_PAGE_TOKENS tokens of ONE kv head:
+ * K rows [0,16) then V rows [0,16), each row FS_HEAD_DIM bf16 (256 B), the
+ * 16-byte chunk c of row r stored at chunk position c ^ (r & 7) (bank-
+ * conflict-free ldmatrix after a linear TMA bulk copy).  8 KiB per page. */
+#define FS_PAGE_TOKENS 16
+#define FS_HEAD_DIM 128
+#define FS_PAGE_BYTES 8192
+#define FS_MAX_Q_PER_KV 8
+
+int fs_abi_version(void);
+const char *fs_last_error(void);
+/* number of SMs of `device` (sizes the stream-K partition), or <0 */
+int fs_device_sms(int device);
+
+/* ---------------------------------------------------------------- host --- */
+
+/* owner[L*H] <- GPU id of each (layer, head), FS_REPLICATED for hybrid's
+ * replicated heads.  alive: n_alive distinct GPU ids (any order). */
+int fs_plan_placement(int mode, int num_layers, int num_kv_heads,
+                      const int32_t *alive, int n_alive, int32_t *owner);
+
+/* shard_owner[num_shards] <- GPU id of each FFN shard */
+int fs_plan_ffn(int num_shards, const int32_t *alive, int n_alive,
+                int32_t *shard_owner);
+
+/* On-demand shrink target: survivors keep their heads/shards, departed
+ * GPUs' TP heads become replicated, lost shards go to the least-loaded
+ * survivor (ties -> lowest id). */
+int fs_plan_on_demand(int num_layers, int num_kv_heads, const int32_t *owner,
+                      int num_shards, const int32_t *shard_owner,
+                      const int32_t *survivors, int n_surv,
+                      int32_t *new_owner, int32_t *new_shard_owner);
+
+/* Per-GPU KV bytes of a placement for given request token counts and
+ * routing (routing[r] = GPU of request r; may be NULL if no replicated
+ * heads).  out_bytes[i] corresponds to alive[i]. */
+int fs_kv_footprint(int num_layers, int num_kv_heads, const int32_t *owner,
+                    const int32_t *alive, int n_alive, const int64_t *tokens,
+                    const int32_t *routing, int n_req, int64_t unit,
+                    int64_t *out_bytes);
+
+/* -------------------------------------------------------------- device --- */
+
+/* K4: page prefix per segment (one segment = one layer's work items).
+ * For segment s with items [seg_items[s], seg_items[s+1]) it writes the
+ * exclusive prefix of ceil(item_len/16) to
+ * page_off[seg_items[s] + s .. seg_items[s+1] + s] (n+1 entries). */
+int fs_plan_pages(const int32_t *item_len, const int32_t *seg_items, int n_segs,
+                  int32_t *page_off, void *stream);
+
+typedef struct fs_decode_desc {
+    const void *q;             /* bf16 [n_qrows][q_per_kv][128]            */
+    const void *kv_pool;       /* pages, FS_PAGE_BYTES each                 */
+    const int32_t *block_table;/* [n_seq][bt_stride] page ids               */
+    int64_t bt_stride;
+    const int32_t *item_seq;   /* [n_items] block-table row                 */
+    const int32_t *item_len;   /* [n_items] tokens attended (>=0)           */
+    const int32_t *item_qrow;  /* [n_items] query row                       */
+    const int32_t *item_orow;  /* [n_items] output row                      */
+    const int32_t *page_off;   /* [n_items+1] from fs_plan_pages            */
+    int32_t n_items;
+    int32_t q_per_kv;          /* 1..8                                      */
+    float scale;               /* softmax scale, normally 1/sqrt(head_dim)  */
+    int32_t out_fp32;          /* 0: bf16 out, 1: fp32 out                  */
+    void *out;                 /* [n_orows][q_per_kv][128]                  */
+    float *part_o;             /* [partial_slots][q_per_kv][128] fp32       */
+    float *part_lse;           /* [partial_slots][q_per_kv]                 */
+    int64_t partial_slots;     /* >= fs_decode_partial_slots(n_items)       */
+    int32_t device;            /* CUDA device ordinal the launch runs on    */
+    int32_t config;            /* 0 = default kernel configuration          */
+} fs_decode_desc;
+
+/* partial-result slots the stream-K split needs for n_items items */
+int64_t fs_decode_partial_slots(int device, int32_t n_items, int32_t config);
+
+/* K1 + K2: split-KV (stream-K over pages) paged GQA decode plus the
+ * log-sum-exp combine.  Output rows not named by any item are untouched. */
+int fs_decode_attention(const fs_decode_desc *d, void *stream);
+
+/* K3: write n_tok (K,V) rows into pages: token t goes to sequence
+ * tok_seq[t] at position tok_pos[t]; its K/V are rows tok_src[t] of
+ * k_src/v_src (bf16, row stride src_stride elements, 128 used). */
+int fs_kv_write(void *kv_pool, const int32_t *block_table, int64_t bt_stride,
+                const int32_t *tok_seq, const int32_t *tok_pos,
+                const int32_t *tok_src, int32_t n_tok, const void *k_src,
+                const void *v_src, int64_t src_stride, void *stream);
+
+/* inverse of fs_kv_write (tests / debugging) */
+int fs_kv_read(const void *kv_pool, const int32_t *block_table, int64_t bt_stride,
+               const int32_t *tok_seq, const int32_t *tok_pos,
+               const int32_t *tok_dst, int32_t n_tok, void *k_dst, void *v_dst,
+               int64_t dst_stride, void *stream);
+
+/* K5: dst[i] <- page page_ids[i] (dst may be mapped pinned host memory) */
+int fs_pages_gather(const void *kv_pool, const int32_t *page_ids, int32_t n_pages,
+                    void *dst, int32_t max_ctas, void *stream);
+
+/* K6: page page_ids[i] <- src[i] (src may be mapped pinned host memory) */
+int fs_pages_scatter(void *kv_pool, const int32_t *page_ids, int32_t n_pages,
+                     const void *src, int32_t max_ctas, void *stream);
+
+/* K7: enable peer access (idempotent) and peer copy */
+int fs_enable_peer(int device, int peer);
+int fs_copy_peer(void *dst, int dst_device, const void *src, int src_device,
+                 int64_t bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FAILSAFE_B200_H */

@@ -1,0 +1,209 @@
+"""GPU parity of K1/K2 (paged GQA decode + combine), K3 (KV write) and K4
+(page planner) against the CPU oracle and the reference golden vectors.
+
+Tolerance (north star): bf16 K/V, fp32 accumulation -> max-abs <= 2e-2 and
+mean-rel <= 1e-3 vs the float64 oracle on the same bf16 inputs, where
+mean-rel = mean|gpu - ref| / mean|ref|.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+MAX_ABS = 2e-2
+MEAN_REL = 1e-3
+
+
+def _close(gpu, ref):
+    gpu = np.asarray(gpu, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    err = np.abs(gpu - ref)
+    max_abs = float(err.max()) if err.size else 0.0
+    mean_rel = float(err.mean() / max(np.abs(ref).mean(), 1e-30)) if err.size else 0.0
+    assert max_abs <= MAX_ABS, (max_abs, mean_rel)
+    assert mean_rel <= MEAN_REL, (max_abs, mean_rel)
+    return max_abs, mean_rel
+
+
+def _bf16(t):
+    return t.to(torch.bfloat16)
+
+
+def _build(owner, rank, routing, lens, qpk, order="shuffled", seed=0, config=0):
+    from paper_2511_14116_b200.kvcache import PagedKVCache, RankWork
+    work = RankWork.build(np.asarray(owner, dtype=np.int32), rank, routing, len(lens))
+    cache = PagedKVCache(work, max(max(lens), 1), qpk, device="cuda", page_order=order,
+                         seed=seed, config=config)
+    cache.set_lengths(lens)
+    return work, cache
+
+
+def _fill(cache, work, lens, gen):
+    """Random bf16 K/V for every (item, position); returns dense copies."""
+    kv = {}
+    seqs, poss, ks, vs = [], [], [], []
+    for i in range(work.n_items):
+        n = lens[work.item_req[i]]
+        k = _bf16(torch.randn((n, 128), generator=gen))
+        v = _bf16(torch.randn((n, 128), generator=gen))
+        kv[i] = (k.double().numpy(), v.double().numpy())
+        seqs.append(np.full(n, i))
+        poss.append(np.arange(n))
+        ks.append(k)
+        vs.append(v)
+    cache.write_tokens(np.concatenate(seqs), np.concatenate(poss),
+                       torch.cat(ks).cuda(), torch.cat(vs).cuda())
+    return kv
+
+
+def _expected(work, kv, q, lens, n_rows):
+    from oracle.attention import head_decode
+    out = np.zeros((n_rows,) + q.shape[1:])
+    for i in range(work.n_items):
+        r, j = work.item_req[i], work.item_slot[i]
+        row = r * work.n_slots + j
+        k, v = kv[i]
+        out[row] = head_decode(q[row], k[:lens[r]], v[:lens[r]], 1.0 / math.sqrt(128))
+    return out
+
+
+@pytest.mark.parametrize("qpk", [1, 4, 8])
+@pytest.mark.parametrize("config", [0, 2])
+def test_decode_hybrid_rank_ragged(qpk, config):
+    """Hybrid N=7 rank: 1 TP head for all requests + 1 DP head for routed
+    requests; ragged lengths incl. 1, page edges and multi-warp items."""
+    from oracle.placement import owner_table
+    owner = owner_table("hybrid", 2, 8, range(7))
+    lens = [1, 15, 16, 17, 33, 300, 1000, 4097, 2]
+    routing = {r: r % 7 for r in range(len(lens))}
+    from oracle.attention import head_decode
+    gen = torch.Generator().manual_seed(qpk * 10 + config)
+    for rank in (0, 3):
+        work, cache = _build(owner, rank, routing, lens, qpk, config=config)
+        kv = _fill(cache, work, lens, gen)
+        n_rows = len(lens) * work.n_slots
+        q = _bf16(torch.randn((n_rows, qpk, 128), generator=gen))
+        qn = q.double().numpy()
+        out = torch.zeros((n_rows, qpk, 128), dtype=torch.float32, device="cuda")
+        q_dev = q.cuda()
+        ref = np.zeros((n_rows, qpk, 128))
+        for layer in range(2):
+            out.zero_()
+            cache.decode_layer(layer, q_dev, out)
+            torch.cuda.synchronize()
+            a, b = work.seg_items[layer], work.seg_items[layer + 1]
+            exp = np.zeros_like(ref)
+            for i in range(a, b):
+                r, j = work.item_req[i], work.item_slot[i]
+                row = r * work.n_slots + j
+                k, v = kv[i]
+                exp[row] = head_decode(qn[row], k[:lens[r]], v[:lens[r]], 1 / math.sqrt(128))
+            _close(out.cpu().numpy(), exp)
+
+
+def test_decode_bf16_output_and_determinism():
+    from oracle.placement import owner_table
+    owner = owner_table("cyclic", 1, 8, range(2))
+    lens = [4096, 777, 64]
+    routing = {r: 0 for r in range(3)}
+    work, cache = _build(owner, 1, routing, lens, 4)
+    gen = torch.Generator().manual_seed(3)
+    kv = _fill(cache, work, lens, gen)
+    n_rows = 3 * work.n_slots
+    q = _bf16(torch.randn((n_rows, 4, 128), generator=gen))
+    o1 = torch.zeros((n_rows, 4, 128), dtype=torch.bfloat16, device="cuda")
+    o2 = torch.zeros_like(o1)
+    cache.decode_layer(0, q.cuda(), o1)
+    cache.decode_layer(0, q.cuda(), o2)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
+    exp = _expected(work, kv, q.double().numpy(), lens, n_rows)
+    # bf16 output rounding adds <= 2^-9 relative; check max-abs only
+    assert float(np.abs(o1.float().cpu().numpy() - exp).max()) <= MAX_ABS
+
+
+def test_decode_reference_golden(golden):
+    """Decode rows of the reference _head_attention (bf16-exact inputs)."""
+    from paper_2511_14116_b200.kvcache import PagedKVCache, RankWork
+    g = golden("decode")
+    for case in g["cases"]:
+        qpk, seq_lens = case["qpk"], case["seq_lens"]
+        x = torch.tensor(case["x"], dtype=torch.float64)
+        owner = np.zeros((1, 1), dtype=np.int32)  # one KV head owned by rank 0
+        work = RankWork.build(owner, 0, {r: 0 for r in range(len(seq_lens))}, len(seq_lens))
+        cache = PagedKVCache(work, max(seq_lens), qpk, page_order="shuffled", seed=1)
+        cache.set_lengths(seq_lens)
+        seqs, poss = [], []
+        start = 0
+        q = torch.zeros((len(seq_lens), qpk, 128), dtype=torch.float64)
+        diag = torch.tensor(case["diag"], dtype=torch.float64)
+        for r, n in enumerate(seq_lens):
+            seqs.append(np.full(n, r))
+            poss.append(np.arange(n))
+            q[r] = x[start + n - 1][None, :] * diag
+            start += n
+        xb = x.to(torch.bfloat16).cuda()
+        assert torch.equal(xb.double().cpu(), x)  # inputs are bf16-exact
+        cache.write_tokens(np.concatenate(seqs), np.concatenate(poss), xb, xb)
+        out = torch.zeros((len(seq_lens), qpk, 128), dtype=torch.float32, device="cuda")
+        cache.decode_layer(0, q.to(torch.bfloat16).cuda(), out)
+        torch.cuda.synchronize()
+        _close(out.cpu().numpy(), np.array(case["out"]))
+
+
+def test_kv_write_read_roundtrip_bitexact():
+    from paper_2511_14116_b200.kvcache import PagedKVCache, RankWork
+    owner = np.zeros((1, 2), dtype=np.int32)
+    work = RankWork.build(owner, 0, {0: 0, 1: 0}, 2)
+    cache = PagedKVCache(work, 100, 1, page_order="shuffled", seed=5)
+    n = 4 * 100
+    seq = np.repeat(np.arange(4), 100)
+    pos = np.tile(np.arange(100), 4)
+    k = torch.randn((n, 128), device="cuda").to(torch.bfloat16)
+    v = torch.randn((n, 128), device="cuda").to(torch.bfloat16)
+    cache.write_tokens(seq, pos, k, v)
+    k2, v2 = cache.read_tokens(seq, pos)
+    assert torch.equal(k, k2) and torch.equal(v, v2)
+    # the page format is swizzled: row r chunk c at c ^ (r & 7)
+    page = cache.block_table[0, 0].item()
+    raw = cache.pool[page].view(torch.bfloat16)[: 16 * 128].view(16, 16, 8)
+    for r in (0, 5, 9):
+        for c in (0, 3, 15):
+            assert torch.equal(raw[r, c ^ (r & 7)], k[r, c * 8:(c + 1) * 8])
+
+
+def test_plan_pages_matches_host_prefix():
+    from paper_2511_14116_b200.kvcache import PagedKVCache, RankWork
+    rng = np.random.default_rng(0)
+    owner = np.array([[0, 0, -1], [0, -1, 0], [-1, -1, -1]], dtype=np.int32)
+    B = 2500
+    lens = rng.integers(0, 70, size=B)
+    routing = {r: int(rng.integers(0, 2)) for r in range(B)}
+    work = RankWork.build(owner, 0, routing, B)
+    cache = PagedKVCache(work, 70, 1)
+    cache.set_lengths(lens)
+    torch.cuda.synchronize()
+    got = cache.page_off.cpu().numpy()
+    for layer in range(3):
+        a, b = work.seg_items[layer], work.seg_items[layer + 1]
+        pages = (lens[work.item_req[a:b]] + 15) // 16
+        exp = np.concatenate([[0], np.cumsum(pages)])
+        assert np.array_equal(got[a + layer:b + layer + 1], exp)
+
+
+def test_decode_errors_map_to_reference_exceptions():
+    from paper_2511_14116_b200 import ValidationError
+    from paper_2511_14116_b200.kvcache import PagedKVCache, RankWork
+    work = RankWork.build(np.zeros((1, 1), np.int32), 0, {0: 0}, 1)
+    with pytest.raises(ValidationError):
+        PagedKVCache(work, 16, 9)
+    cache = PagedKVCache(work, 16, 2)
+    cache.qpk = 9
+    cache.set_lengths([3])
+    with pytest.raises(ValidationError):
+        cache.decode_layer(0, torch.zeros((1, 9, 128), dtype=torch.bfloat16, device="cuda"),
+                           torch.zeros((1, 9, 128), dtype=torch.bfloat16, device="cuda"))
