@@ -1,0 +1,483 @@
+#!/usr/bin/env python
+"""bench.py -- FailSafe (arXiv 2511.14116) hybrid-attention decode on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N=1 (default) runs BASELINE config 2 -- the Llama-3-8B-shaped hybrid-
+attention decode step, batch 64, context 4096, hybrid placement -- on one
+GPU; N>1 (torchrun, one process per GPU, NCCL) runs the same job split over
+N ranks (hybrid placement, least-loaded routing, NCCL all-reduce of the
+attention output).  One JSON line on rank 0.
+
+A *step* = one decode token for all 64 requests through every layer's
+attention sublayer: fused QKV GEMM (cuBLAS) -> ONE fs_decode_attention launch
+(KV append + paged GQA decode + split merge) -> output projection ->
+exchange (NCCL all-reduce when N>1) -> residual.  The whole step is one
+CUDA-graph replay.  The KV working set (34 GB at N=1) is far larger than L2,
+so no flush is needed between steps.
+
+At N=1 the line also carries (rank 0 only):
+* ``failure_states`` -- BASELINE config 3 (Llama-3-70B-shaped, B=64,
+  ctx 4096) at the 8 -> 7 -> 6 -> 5 on-demand shrink chain, every rank of
+  every world emulated on this GPU (exchange excluded: one GPU);
+* ``recovery`` -- config 4 microbenchmark (KV restore from the pinned host
+  backup, weight shards) after 1-3 losses;
+* ``cpu_baseline`` -- the CPU oracle port on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("decode tokens/s at 8→7→6→5 B200 (fraction of HBM roofline); "
+          "failure recovery ms")
+UNIT = "tokens/s"
+KV_UNIT = 512  # bytes per (kv head, token): K+V, head_dim 128, bf16 (core.py:101-103)
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ----------------------------------------------------------------- clocks --
+class ClockSampler:
+    """Samples SM clock + throttle reasons with NVML every 10 ms."""
+
+    HW = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+          "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self._nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+            return self
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                pass
+            self._stop.wait(0.01)
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"],
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": [k for k, bit in self.HW.items() if self.reasons & bit],
+                "samples": len(self.samples)}
+
+
+# -------------------------------------------------------------- workloads --
+def llama8b():
+    from paper_2511_14116_b200.core import ModelSpec
+    return ModelSpec(num_layers=32, num_kv_heads=8, num_q_heads=32, head_dim=128,
+                     hidden_dim=4096, ffn_intermediate_dim=14336)
+
+
+def llama70b():
+    from paper_2511_14116_b200.core import load_config
+    return load_config(os.path.join(ROOT, "paper_2511_14116_b200", "data", "llama70b.toml"))[0]
+
+
+def route(n_requests, ranks, ctx):
+    """Least-loaded routing of equal requests (scheduler.py:160-164)."""
+    from paper_2511_14116_b200.core import Request
+    from paper_2511_14116_b200.scheduler import SchedulerState, route_request
+    st = SchedulerState(token_budget=2048, rank_set=tuple(ranks))
+    return {i: route_request(st, Request(id=i, arrival_time=0.0, input_len=ctx - 1,
+                                         output_len=1)) for i in range(n_requests)}
+
+
+def build_rank(model, owner, rank, routing, batch, ctx, group, config, seed=0):
+    import torch
+    from paper_2511_14116_b200.hybrid import HybridDecodeRank
+    eng = HybridDecodeRank(model, owner, rank, routing, batch, ctx, group=group, seed=seed,
+                           config=config)
+    eng.set_lengths([ctx] * batch)
+    eng.fill_random_kv(seed + 17 * rank)
+    eng.x.copy_(torch.randn_like(eng.x, dtype=torch.float32).to(torch.bfloat16))
+    eng.capture()
+    return eng
+
+
+def time_graph(fn, steps, warmup, stream=None):
+    """Device time (ms per call) of ``fn`` with CUDA events on the current
+    stream, synchronized on both sides."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / steps
+
+
+def attention_op_graph(eng):
+    """A CUDA graph of just the per-layer fs_decode_attention launches."""
+    import torch
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for layer in range(eng.model.num_layers):
+            eng.cache.decode_layer_fused(layer, eng.qkv, eng.o)
+    return g
+
+
+def step_kv_bytes(eng):
+    return sum(eng.cache.layer_kv_bytes(l) for l in range(eng.model.num_layers))
+
+
+def ncu_traffic():
+    """dram bytes per decode launch from the committed ncu --set full
+    summary (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_decode_summary.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get("dram_bytes_per_launch"), d
+    except Exception:
+        return None, None
+
+
+# ------------------------------------------------------- failure states --
+def failure_states(steps, warmup, config, batch=64, ctx=4096, fails=(7, 3, 5)):
+    import torch
+    from paper_2511_14116_b200 import _native as N
+    from paper_2511_14116_b200.placement import (make_placement, memory_footprint,
+                                                 owner_array)
+    from paper_2511_14116_b200.recovery import plan_weight_recovery
+    model = llama70b()
+    peak, _ = measured_peaks()
+    plan = make_placement("hybrid", model, range(8))
+    alive = list(range(8))
+    states = []
+    chain = [None] + list(fails)
+    for f in chain:
+        if f is not None:
+            alive = [g for g in alive if g != f]
+            plan = plan_weight_recovery(model, plan, alive, "on_demand").target_plan(
+                "hybrid", model)
+        owner = owner_array(plan, model.num_kv_heads)
+        routing = route(batch, alive, ctx)
+        fp = memory_footprint(plan, model, {r: ctx for r in range(batch)}, routing)
+        per_rank = []
+        for g in alive:
+            eng = build_rank(model, owner, g, routing, batch, ctx, None, config)
+            ms = time_graph(eng.step, min(steps, 20), warmup)
+            kb = step_kv_bytes(eng)
+            att = attention_op_graph(eng)
+            att_ms = time_graph(att.replay, min(steps, 20), 2)
+            per_rank.append({"rank": g, "step_ms": round(ms, 4), "kv_bytes": kb,
+                             "attn_ms": round(att_ms, 4),
+                             "attn_gbs": round(kb / att_ms / 1e6, 1)})
+            del eng, att
+            torch.cuda.empty_cache()
+        worst = max(per_rank, key=lambda r: r["step_ms"])
+        states.append({
+            "world": len(alive), "failed": f, "max_rank_step_ms": worst["step_ms"],
+            "tok_s": round(batch / (worst["step_ms"] / 1e3), 1),
+            "max_kv_bytes": max(fp.values()),
+            "kv_roofline_frac": round(max(fp.values()) / (worst["step_ms"] / 1e3) / 1e9 / peak, 4),
+            "attn_frac_min": round(min(r["attn_gbs"] for r in per_rank) / peak, 4),
+            "ranks": per_rank})
+    r8 = states[0]["tok_s"]
+    out = {"workload": "C3 Llama-3-70B-shaped attention, B=64, ctx 4096, hybrid(8) then "
+                       "on-demand shrink after failures of GPU 7, 3, 5",
+           "emulation": "every rank of every world timed on this one GPU (graph replay); "
+                        "step = max over ranks; the NCCL exchange is excluded (1 GPU)",
+           "states": states}
+    for s in states[1:]:
+        s["vs_8_scaled"] = round(s["tok_s"] / (r8 * s["world"] / 8), 4)
+    return out
+
+
+# ------------------------------------------------------------ CPU oracle --
+def cpu_oracle_rate(qpk, ctx, seconds=8.0):
+    """Items/s of the oracle port (float64 numpy decode of one (kv head,
+    request) item, refexec.py:85-103) on all host cores, one thread per
+    item; returns (items_per_s, cores, items_done)."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle.attention import head_decode
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:  # pragma: no cover
+        threadpool_limits = None
+    cores = len(os.sched_getaffinity(0))
+    rng = np.random.default_rng(0)
+    k = rng.standard_normal((ctx, 128)).astype(np.float32)
+    v = rng.standard_normal((ctx, 128)).astype(np.float32)
+    qs = [rng.standard_normal((qpk, 128)).astype(np.float32) for _ in range(cores)]
+    scale = 1.0 / np.sqrt(128)
+    done = [0] * cores
+    stop = time.perf_counter() + seconds
+
+    def worker(i):
+        while time.perf_counter() < stop:
+            head_decode(qs[i], k, v, scale)
+            done[i] += 1
+
+    ctx_mgr = threadpool_limits(1) if threadpool_limits else None
+    t0 = time.perf_counter()
+    if ctx_mgr:
+        ctx_mgr.__enter__()
+    try:
+        with ThreadPoolExecutor(cores) as ex:
+            list(ex.map(worker, range(cores)))
+    finally:
+        if ctx_mgr:
+            ctx_mgr.__exit__(None, None, None)
+    dt = time.perf_counter() - t0
+    return sum(done) / dt, cores, sum(done)
+
+
+def job_items(model, world, batch, ctx):
+    """Work items (kv head, request) of one step over all ranks."""
+    import numpy as np
+    from paper_2511_14116_b200.placement import make_placement, owner_array
+    plan = make_placement("hybrid", model, range(world))
+    owner = owner_array(plan, model.num_kv_heads)
+    routing = route(batch, range(world), ctx)
+    n = 0
+    for row in owner:
+        tp = int((row >= 0).sum())
+        dp = int((row < 0).sum())
+        n += tp * batch + dp * batch  # every request once per head
+    return n
+
+
+# ---------------------------------------------------------------- drivers --
+def run_reference(args, world, rank):
+    """--impl reference: the reference's CPU path for the hot path (the
+    oracle port of refexec._head_attention -- the reference itself is pure
+    Python/numpy and not present on the GPU box) on this host's cores."""
+    if rank != 0:
+        return
+    model = llama8b()
+    batch, ctx = 64, 4096
+    items = job_items(model, world, batch, ctx)
+    per_step = []
+    for i in range(args.warmup + args.steps):
+        rate, cores, done = cpu_oracle_rate(model.q_heads_per_kv_head, ctx,
+                                            seconds=args.ref_seconds)
+        if i >= args.warmup:
+            per_step.append(items / rate)
+    step_s = statistics.median(per_step)
+    value = batch / step_s
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(step_s * 1e3, 1), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(model, world, batch, ctx),
+            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores,
+                             "kind": "port",
+                             "sample": f"each step: {args.ref_seconds:.0f}s of float64 numpy "
+                                       f"decode items (qpk 4, ctx {ctx}) on {cores} threads, "
+                                       f"extrapolated to the {items} items of one step"},
+            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(model, world, batch, ctx):
+    return {"workload": "C2 Llama-3-8B-shaped hybrid-attention decode step "
+                        "(QKV GEMM, fused KV-append + paged GQA decode, O GEMM, "
+                        "NCCL all-reduce when N>1)",
+            "layers": model.num_layers, "q_heads": model.num_q_heads,
+            "kv_heads": model.num_kv_heads, "head_dim": model.head_dim,
+            "hidden": model.hidden_dim, "batch": batch, "ctx": ctx, "world": world,
+            "placement": "hybrid", "page_tokens": 16, "parallelism": f"hybrid-tp{world}",
+            "l2": "no flush: KV working set >> 126 MB L2 (34 GB at N=1)"}
+
+
+def run_ours(args, world, rank, local_rank):
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    group = dist.group.WORLD if world > 1 else None
+    model = llama8b()
+    batch, ctx = 64, 4096
+    from paper_2511_14116_b200.placement import make_placement, owner_array
+    plan = make_placement("hybrid", model, range(world))
+    owner = owner_array(plan, model.num_kv_heads)
+    routing = route(batch, range(world), ctx)
+    eng = build_rank(model, owner, rank, routing, batch, ctx, group, args.kernel_config)
+    peak, peak_src = measured_peaks()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- value: resident inputs, graph replay, CUDA events ----
+    for _ in range(args.warmup):
+        eng.step()
+    barrier()
+    with ClockSampler(local_rank) as clk:
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(args.steps):
+            eng.step()
+        e.record()
+        barrier()
+        ms = s.elapsed_time(e) / args.steps
+    ms = max_over_ranks(ms)
+    value = batch / (ms / 1e3)
+
+    # ---- e2e: public API, pinned host x in, result back to host ----
+    x_host = torch.randn((batch, model.hidden_dim)).to(torch.bfloat16).pin_memory()
+    y_host = torch.empty_like(x_host).pin_memory()
+    for _ in range(2):
+        y_host.copy_(eng.step(x_host))
+        torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        y_host.copy_(eng.step(x_host))   # H2D inside step(), D2H read of the result
+        torch.cuda.current_stream().synchronize()
+    e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / args.steps)
+    nbytes = x_host.numel() * 2
+
+    # ---- roofline: the fused decode launches alone ----
+    att = attention_op_graph(eng)
+    att_ms = time_graph(att.replay, max(3, args.steps), 3)
+    kv_step = step_kv_bytes(eng)
+    per_launch_bytes = kv_step / model.num_layers
+    per_launch_ms = att_ms / model.num_layers
+    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
+    traffic, _ = ncu_traffic()
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": "decode_kernel (fs_decode_attention: fused KV append + paged GQA "
+                          "decode + in-kernel split merge), one launch per layer",
+                "bytes_per_launch": int(per_launch_bytes),
+                "launch_ms": round(per_launch_ms, 5), "peak_source": peak_src,
+                "step_kv_frac": round(kv_step / (ms / 1e3) / 1e9 / peak, 4)}
+    del att
+
+    line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (seeded random weights and KV)",
+            "config": workload_config(model, world, batch, ctx),
+            "e2e": {"value": round(batch / (e2e_ms / 1e3), 1), "unit": UNIT,
+                    "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                    "ms_per_step": round(e2e_ms, 4),
+                    "api": "HybridDecodeRank.step(x_pinned_host) + D2H of x"},
+            "roofline": roofline, "clocks": clk.summary(),
+            "gpu_launches": eng.launches_per_step() * args.steps}
+    del eng
+    torch.cuda.empty_cache()
+
+    if world == 1 and rank == 0:
+        if not args.skip_failure_states:
+            line["failure_states"] = failure_states(args.steps, args.warmup, args.kernel_config)
+        if not args.skip_recovery:
+            try:
+                from paper_2511_14116_b200.recovery_exec import recovery_microbench
+                line["recovery"] = recovery_microbench()
+            except ImportError:
+                pass
+        if not args.skip_cpu:
+            rate, cores, done = cpu_oracle_rate(model.q_heads_per_kv_head, ctx,
+                                                seconds=args.cpu_seconds)
+            items = job_items(model, world, batch, ctx)
+            line["cpu_baseline"] = {
+                "value": round(batch / (items / rate), 4), "unit": UNIT, "cores": cores,
+                "kind": "port",
+                "sample": f"{done} float64 numpy decode items (qpk 4, ctx {ctx}) in "
+                          f"{args.cpu_seconds:.0f}s on {cores} threads, extrapolated to the "
+                          f"{items} items of one step"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--kernel-config", type=int, default=0)
+    ap.add_argument("--skip-failure-states", action="store_true")
+    ap.add_argument("--skip-recovery", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--ref-seconds", type=float, default=4.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            ap.error("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, world, rank, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -113,20 +113,28 @@ int fs_plan_pages(const int32_t *item_len, const int32_t *seg_items, int n_segs,
                   int32_t *page_off, void *stream);
 
 typedef struct fs_decode_desc {
-    const void *q;             /* bf16 [n_qrows][q_per_kv][128]            */
+    const void *q;             /* bf16; item i's q_per_kv x 128 query block
+                                  starts at element item_qoff[i]            */
     const void *kv_pool;       /* pages, FS_PAGE_BYTES each                 */
     const int32_t *block_table;/* [n_seq][bt_stride] page ids               */
     int64_t bt_stride;
     const int32_t *item_seq;   /* [n_items] block-table row                 */
-    const int32_t *item_len;   /* [n_items] tokens attended (>=0)           */
-    const int32_t *item_qrow;  /* [n_items] query row                       */
-    const int32_t *item_orow;  /* [n_items] output row                      */
+    const int32_t *item_len;   /* [n_items] tokens attended (>=0), incl. the
+                                  new token at position len-1               */
+    const int32_t *item_qoff;  /* [n_items] element offset into q           */
+    const int32_t *item_ooff;  /* [n_items] element offset into out         */
     const int32_t *page_off;   /* [n_items+1] from fs_plan_pages            */
+    const void *kv_new;        /* bf16 new-token K/V source, or NULL: when
+                                  set, the token at len-1 is first written
+                                  into its page (fused KV append)           */
+    const int32_t *item_koff;  /* [n_items] element offset of the new K row */
+    const int32_t *item_voff;  /* [n_items] element offset of the new V row */
+    int32_t *item_sem;         /* [n_items] zero-initialised; left zero     */
     int32_t n_items;
     int32_t q_per_kv;          /* 1..8                                      */
     float scale;               /* softmax scale, normally 1/sqrt(head_dim)  */
     int32_t out_fp32;          /* 0: bf16 out, 1: fp32 out                  */
-    void *out;                 /* [n_orows][q_per_kv][128]                  */
+    void *out;                 /* q_per_kv x 128 block per item at ooff     */
     float *part_o;             /* [partial_slots][q_per_kv][128] fp32       */
     float *part_lse;           /* [partial_slots][q_per_kv]                 */
     int64_t partial_slots;     /* >= fs_decode_partial_slots(n_items)       */
@@ -134,11 +142,14 @@ typedef struct fs_decode_desc {
     int32_t config;            /* 0 = default kernel configuration          */
 } fs_decode_desc;
 
-/* partial-result slots the stream-K split needs for n_items items */
+/* partial-result slots the stream-K split needs for n_items items
+ * (config -1: enough for every kernel configuration) */
 int64_t fs_decode_partial_slots(int device, int32_t n_items, int32_t config);
 
-/* K1 + K2: split-KV (stream-K over pages) paged GQA decode plus the
- * log-sum-exp combine.  Output rows not named by any item are untouched. */
+/* K1 (+ fused K2 combine, + optional fused K3 append): split-KV (stream-K
+ * over pages) paged GQA decode with the log-sum-exp merge of split items
+ * done in-kernel by the item's last warp.  ONE launch.  Output blocks not
+ * named by any item are untouched. */
 int fs_decode_attention(const fs_decode_desc *d, void *stream);
 
 /* K3: write n_tok (K,V) rows into pages: token t goes to sequence

@@ -33,8 +33,9 @@ class DecodeDesc(C.Structure):
     _fields_ = [
         ("q", C.c_void_p), ("kv_pool", C.c_void_p), ("block_table", C.c_void_p),
         ("bt_stride", C.c_int64), ("item_seq", C.c_void_p), ("item_len", C.c_void_p),
-        ("item_qrow", C.c_void_p), ("item_orow", C.c_void_p), ("page_off", C.c_void_p),
-        ("n_items", C.c_int32), ("q_per_kv", C.c_int32), ("scale", C.c_float),
+        ("item_qoff", C.c_void_p), ("item_ooff", C.c_void_p), ("page_off", C.c_void_p),
+        ("kv_new", C.c_void_p), ("item_koff", C.c_void_p), ("item_voff", C.c_void_p),
+        ("item_sem", C.c_void_p), ("n_items", C.c_int32), ("q_per_kv", C.c_int32), ("scale", C.c_float),
         ("out_fp32", C.c_int32), ("out", C.c_void_p), ("part_o", C.c_void_p),
         ("part_lse", C.c_void_p), ("partial_slots", C.c_int64), ("device", C.c_int32),
         ("config", C.c_int32),

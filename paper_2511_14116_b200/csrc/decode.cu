@@ -1,23 +1,31 @@
-// K1 / K2 / K4: stream-K paged GQA decode for the FailSafe hybrid-attention
-// step (the attention half of refexec.parallel_forward, refexec.py:281-297,
-// with the per-head math of _head_attention, refexec.py:85-103).
+// K1 (+ fused K2 combine and K3 append) and K4 of the FailSafe B200 hot
+// path: a stream-K paged GQA decode for the hybrid-attention step (the
+// attention half of refexec.parallel_forward, refexec.py:281-297, with the
+// per-head math of _head_attention, refexec.py:85-103).
 //
-// Work = a list of items (one per (kv head, request) pair a rank serves:
+// Work = a list of items, one per (kv head, request) pair a rank serves:
 // every request for its TP heads, only routed requests for replicated
-// heads).  All items' pages are flattened into one page space of P pages
-// and split EVENLY over every warp of a persistent grid (W = SMs x WARPS):
-// warp w owns pages [w*P/W, (w+1)*P/W).  A warp streams its pages through
-// a private ring of STAGES x 8 KiB shared-memory slots filled by TMA bulk
-// copies (one cp.async.bulk per page, mbarrier completion), so the HBM
-// pipeline never drains at item boundaries and ragged lengths cost nothing
-// in balance.  Per 16-token page the warp runs
+// heads.  All items' pages are flattened into one page space of P pages
+// and split EVENLY over every warp of a persistent grid (W = SMs x CTAS x
+// WARPS): warp w owns pages [w*P/W, (w+1)*P/W).  A warp streams its pages
+// through a private ring of STAGES x 8 KiB shared-memory slots filled by TMA
+// bulk copies (one cp.async.bulk per page, mbarrier completion), so the
+// HBM pipeline never drains at item boundaries and ragged lengths cost
+// nothing in balance.  Per 16-token page the warp runs
 //     S^T[16 tok x 8 q]   = K[16 x 128]   . Q^T[128 x 8]   (8 mma.m16n8k16)
 //     O^T[128 dim x 8 q] += V^T[128 x 16] . P^T[16 x 8]    (8 mma.m16n8k16)
 // i.e. tensor cores for the GQA query-group tile (q_per_kv <= 8 queries as
 // the mma N dimension), online softmax on the S^T fragments, and P^T made
-// from S^T with movmatrix.trans.  A warp that covers a whole item writes
-// the normalized output; otherwise it writes (O/l, lse) to a partial slot
-// `item + w` and K2 merges the slots of that item.
+// from S^T with movmatrix.trans.
+//
+// Fusions (one launch per layer):
+//  * append: the warp holding the page of position len-1 patches the new
+//    token's K/V (from the projection output) into the landed smem page and
+//    writes it to HBM -- no separate KV-append launch;
+//  * combine: a warp covering a whole item writes the normalized output;
+//    otherwise it writes (O/l, lse) to partial slot `item + w`, bumps the
+//    item's semaphore, and the LAST warp of the item merges the slots and
+//    resets the semaphore to 0 (self-cleaning across launches).
 #include <cuda_bf16.h>
 #include <cub/block/block_scan.cuh>
 
@@ -30,7 +38,10 @@ struct DecodeParams {
     const uint8_t *kv;
     const int32_t *bt;
     int64_t bt_stride;
-    const int32_t *item_seq, *item_len, *item_qrow, *item_orow, *page_off;
+    const int32_t *item_seq, *item_len, *item_qoff, *item_ooff, *page_off;
+    const __nv_bfloat16 *kv_new;            // nullptr: no fused append
+    const int32_t *item_koff, *item_voff;
+    int32_t *item_sem;
     int32_t n_items;
     int32_t qpk;
     float scale_log2;
@@ -44,18 +55,108 @@ __device__ __forceinline__ int64_t owner_warp(int64_t x, int64_t W, int64_t P) {
     return ((x + 1) * W + P - 1) / P - 1;
 }
 
+__device__ __forceinline__ bool warp_live(int64_t w, int64_t W, int64_t P) {
+    return w * P / W < (w + 1) * P / W;
+}
+
 // largest i in [0, n) with off[i] <= x (off is nondecreasing, off[n] > x)
 __device__ __forceinline__ int find_item(const int32_t *off, int n, int64_t x) {
     int lo = 0, hi = n;  // invariant: off[lo] <= x < off[hi]
     while (hi - lo > 1) {
-        int mid = (lo + hi) >> 1;
+        const int mid = (lo + hi) >> 1;
         if (off[mid] <= x) lo = mid; else hi = mid;
     }
     return lo;
 }
 
-template <int WARPS, int STAGES>
-__global__ void __launch_bounds__(WARPS * 32, 1) decode_kernel(const DecodeParams p) {
+__device__ __forceinline__ void store_out(const DecodeParams &p, int64_t idx, float v) {
+    if (p.out_fp32) static_cast<float *>(p.out)[idx] = v;
+    else static_cast<__nv_bfloat16 *>(p.out)[idx] = __float2bfloat16_rn(v);
+}
+
+// merge the partial slots of `item` (called by its last-finishing warp).
+// Lanes first scan the segments in parallel (lse max / weights per query),
+// then stream the partial blocks with 8-16 independent float4 loads in
+// flight per lane; the merge sits on the kernel tail, so it is latency-
+// optimised rather than bandwidth-optimised.
+__device__ __forceinline__ void combine_item(const DecodeParams &p, int item, int64_t wlo,
+                                          int64_t whi, int64_t P, int lane) {
+    const int qpk = p.qpk;
+    const bool all_live = P >= p.n_warps;  // every warp owns >= 1 page
+    const int nseg = (int)(whi - wlo + 1);
+    const float *lse = p.part_lse + (item + wlo) * qpk;
+    const float4 *po = reinterpret_cast<const float4 *>(p.part_o + (item + wlo) * qpk * kHeadDim);
+    float mx[FS_MAX_Q_PER_KV], den[FS_MAX_Q_PER_KV];
+    float4 acc[FS_MAX_Q_PER_KV];
+#pragma unroll
+    for (int q = 0; q < FS_MAX_Q_PER_KV; ++q) {
+        mx[q] = -INFINITY;
+        den[q] = 0.f;
+        acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int base = 0; base < nseg; base += 32) {
+        const int k = base + lane;
+        const bool ok = k < nseg && (all_live || warp_live(wlo + k, p.n_warps, P));
+#pragma unroll
+        for (int q = 0; q < FS_MAX_Q_PER_KV; ++q)
+            if (q < qpk && ok) mx[q] = fmaxf(mx[q], __ldcg(lse + k * qpk + q));
+    }
+#pragma unroll
+    for (int q = 0; q < FS_MAX_Q_PER_KV; ++q)
+        for (int sh = 1; sh < 32; sh <<= 1)
+            mx[q] = fmaxf(mx[q], __shfl_xor_sync(0xffffffffu, mx[q], sh));
+    for (int base = 0; base < nseg; base += 32) {
+        const int k = base + lane;
+        const bool ok = k < nseg && (all_live || warp_live(wlo + k, p.n_warps, P));
+        float wt[FS_MAX_Q_PER_KV];
+#pragma unroll
+        for (int q = 0; q < FS_MAX_Q_PER_KV; ++q) {
+            wt[q] = (q < qpk && ok) ? fast_exp2(__ldcg(lse + k * qpk + q) - mx[q]) : 0.f;
+            den[q] += wt[q];
+        }
+        const unsigned live_mask = __ballot_sync(0xffffffffu, ok);
+        const int cnt = min(32, nseg - base);
+#pragma unroll 2
+        for (int j = 0; j < cnt; ++j) {
+            if (!((live_mask >> j) & 1u)) continue;  // warp-uniform
+            const float4 *blk = po + (int64_t)(base + j) * qpk * (kHeadDim / 4) + lane;
+#pragma unroll
+            for (int q = 0; q < FS_MAX_Q_PER_KV; ++q) {
+                if (q < qpk) {
+                    const float w = __shfl_sync(0xffffffffu, wt[q], j);
+                    const float4 v = __ldcg(blk + q * (kHeadDim / 4));
+                    acc[q].x += w * v.x;
+                    acc[q].y += w * v.y;
+                    acc[q].z += w * v.z;
+                    acc[q].w += w * v.w;
+                }
+            }
+        }
+    }
+    const int64_t ob = p.item_ooff[item];
+#pragma unroll
+    for (int q = 0; q < FS_MAX_Q_PER_KV; ++q) {
+        if (q >= qpk) break;
+        float d = den[q];
+        for (int sh = 1; sh < 32; sh <<= 1) d += __shfl_xor_sync(0xffffffffu, d, sh);
+        const float inv = 1.f / d;
+        const int64_t o = ob + q * kHeadDim + lane * 4;
+        if (p.out_fp32) {
+            *reinterpret_cast<float4 *>(static_cast<float *>(p.out) + o) =
+                make_float4(acc[q].x * inv, acc[q].y * inv, acc[q].z * inv, acc[q].w * inv);
+        } else {
+            __nv_bfloat162 lo = __floats2bfloat162_rn(acc[q].x * inv, acc[q].y * inv);
+            __nv_bfloat162 hi = __floats2bfloat162_rn(acc[q].z * inv, acc[q].w * inv);
+            uint2 pk;
+            pk.x = *reinterpret_cast<uint32_t *>(&lo);
+            pk.y = *reinterpret_cast<uint32_t *>(&hi);
+            *reinterpret_cast<uint2 *>(static_cast<__nv_bfloat16 *>(p.out) + o) = pk;
+        }
+    }
+}
+
+template <int WARPS, int STAGES, int CTAS>
+__global__ void __launch_bounds__(WARPS * 32, CTAS) decode_kernel(const DecodeParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
@@ -66,8 +167,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_kernel(const DecodeParam
     const int64_t x0 = w * P / W, x1 = (w + 1) * P / W;
     if (x0 >= x1) return;  // warp-uniform; no CTA-wide barriers below
 
-    const uint32_t buf0 = smem_u32(smem) + warp * STAGES * kPageBytes;
-    const uint32_t bar0 = smem_u32(smem) + WARPS * STAGES * kPageBytes + warp * STAGES * 8;
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t buf0 = sbase + warp * STAGES * kPageBytes;
+    const uint32_t bar0 = sbase + WARPS * STAGES * kPageBytes + warp * STAGES * 8;
     if (lane == 0) {
         for (int s = 0; s < STAGES; ++s) mbar_init(bar0 + 8 * s, 1);
         fence_barrier_init();
@@ -104,7 +206,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_kernel(const DecodeParam
     float o[8][4];
 
     auto load_q = [&]() {
-        const __nv_bfloat16 *qb = p.q + ((int64_t)p.item_qrow[item] * p.qpk + gid) * kHeadDim;
+        const __nv_bfloat16 *qb = p.q + p.item_qoff[item] + gid * kHeadDim;
         const bool ok = gid < p.qpk;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
@@ -123,14 +225,31 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_kernel(const DecodeParam
     for (int64_t x = x0; x < x1; ++x) {
         const uint32_t kb = buf0 + stage * kPageBytes;
         const uint32_t vb = kb + kHalfPage;
-        const int valid = min(kPageTokens, len - (int)(x - item_begin) * kPageTokens);
+        const int pidx = (int)(x - item_begin);
+        const int valid = min(kPageTokens, len - pidx * kPageTokens);
         mbar_wait(bar0 + 8 * stage, phase);
-        if (valid < kPageTokens) {
-            // tail page: rows >= valid may hold stale bytes; zero the V rows
-            // so 0-probability tokens cannot inject NaN/Inf into P.V
-            uint8_t *vrow = smem + (vb - smem_u32(smem));
-            for (int c = valid * 16 + lane; c < kPageTokens * 16; c += 32)
-                reinterpret_cast<uint4 *>(vrow)[c] = make_uint4(0, 0, 0, 0);
+        const bool tail = valid < kPageTokens;
+        const bool append = p.kv_new != nullptr && valid > 0 &&
+                            (len - 1) / kPageTokens == pidx;
+        if (tail | append) {
+            uint8_t *page_s = smem + (kb - sbase);
+            if (tail) {
+                // rows >= valid may hold stale bytes; zero the V rows so
+                // 0-probability tokens cannot inject NaN/Inf into P.V
+                for (int c = valid * 16 + lane; c < kPageTokens * 16; c += 32)
+                    reinterpret_cast<uint4 *>(page_s + kHalfPage)[c] = make_uint4(0, 0, 0, 0);
+            }
+            if (append) {
+                // fused K3: the new token (position len-1) from the
+                // projection output into the landed page (smem) and HBM
+                const uint32_t r = (len - 1) % kPageTokens, c = lane & 15, half = lane >> 4;
+                const int64_t src = (half ? p.item_voff[item] : p.item_koff[item]) + c * 8;
+                const uint4 v = *reinterpret_cast<const uint4 *>(p.kv_new + src);
+                const uint32_t ofs = half * kHalfPage + swz(r, c);
+                *reinterpret_cast<uint4 *>(page_s + ofs) = v;
+                const int64_t pg = p.bt[(int64_t)p.item_seq[item] * p.bt_stride + pidx];
+                *reinterpret_cast<uint4 *>(const_cast<uint8_t *>(p.kv) + pg * kPageBytes + ofs) = v;
+            }
             fence_proxy_async();
             __syncwarp();
         }
@@ -210,30 +329,17 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_kernel(const DecodeParam
             const int q0 = 2 * tig, q1 = 2 * tig + 1;
             const bool whole = seg_begin == item_begin && x + 1 == item_end;
             if (whole) {
-                const int64_t ob = (int64_t)p.item_orow[item] * p.qpk * kHeadDim;
+                const int64_t ob = p.item_ooff[item];
 #pragma unroll
                 for (int mt = 0; mt < 8; ++mt) {
                     const int d0 = mt * 16 + gid, d1 = d0 + 8;
-                    if (p.out_fp32) {
-                        float *out = static_cast<float *>(p.out) + ob;
-                        if (q0 < p.qpk) {
-                            out[q0 * kHeadDim + d0] = o[mt][0] * inv0;
-                            out[q0 * kHeadDim + d1] = o[mt][2] * inv0;
-                        }
-                        if (q1 < p.qpk) {
-                            out[q1 * kHeadDim + d0] = o[mt][1] * inv1;
-                            out[q1 * kHeadDim + d1] = o[mt][3] * inv1;
-                        }
-                    } else {
-                        __nv_bfloat16 *out = static_cast<__nv_bfloat16 *>(p.out) + ob;
-                        if (q0 < p.qpk) {
-                            out[q0 * kHeadDim + d0] = __float2bfloat16_rn(o[mt][0] * inv0);
-                            out[q0 * kHeadDim + d1] = __float2bfloat16_rn(o[mt][2] * inv0);
-                        }
-                        if (q1 < p.qpk) {
-                            out[q1 * kHeadDim + d0] = __float2bfloat16_rn(o[mt][1] * inv1);
-                            out[q1 * kHeadDim + d1] = __float2bfloat16_rn(o[mt][3] * inv1);
-                        }
+                    if (q0 < p.qpk) {
+                        store_out(p, ob + q0 * kHeadDim + d0, o[mt][0] * inv0);
+                        store_out(p, ob + q0 * kHeadDim + d1, o[mt][2] * inv0);
+                    }
+                    if (q1 < p.qpk) {
+                        store_out(p, ob + q1 * kHeadDim + d0, o[mt][1] * inv1);
+                        store_out(p, ob + q1 * kHeadDim + d1, o[mt][3] * inv1);
                     }
                 }
             } else {
@@ -243,17 +349,35 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_kernel(const DecodeParam
                 for (int mt = 0; mt < 8; ++mt) {
                     const int d0 = mt * 16 + gid, d1 = d0 + 8;
                     if (q0 < p.qpk) {
-                        po[q0 * kHeadDim + d0] = o[mt][0] * inv0;
-                        po[q0 * kHeadDim + d1] = o[mt][2] * inv0;
+                        __stcg(po + q0 * kHeadDim + d0, o[mt][0] * inv0);
+                        __stcg(po + q0 * kHeadDim + d1, o[mt][2] * inv0);
                     }
                     if (q1 < p.qpk) {
-                        po[q1 * kHeadDim + d0] = o[mt][1] * inv1;
-                        po[q1 * kHeadDim + d1] = o[mt][3] * inv1;
+                        __stcg(po + q1 * kHeadDim + d0, o[mt][1] * inv1);
+                        __stcg(po + q1 * kHeadDim + d1, o[mt][3] * inv1);
                     }
                 }
                 if (gid == 0) {
-                    if (q0 < p.qpk) p.part_lse[slot * p.qpk + q0] = m0 + __log2f(t0);
-                    if (q1 < p.qpk) p.part_lse[slot * p.qpk + q1] = m1 + __log2f(t1);
+                    if (q0 < p.qpk) __stcg(p.part_lse + slot * p.qpk + q0, m0 + __log2f(t0));
+                    if (q1 < p.qpk) __stcg(p.part_lse + slot * p.qpk + q1, m1 + __log2f(t1));
+                }
+                // publish, count, and let the last warp of the item merge
+                __threadfence();
+                __syncwarp();
+                int prev = 0;
+                if (lane == 0) prev = atomicAdd(p.item_sem + item, 1);
+                prev = __shfl_sync(0xffffffffu, prev, 0);
+                const int64_t wlo = owner_warp(item_begin, W, P);
+                const int64_t whi = owner_warp(item_end - 1, W, P);
+                int nseg = (int)(whi - wlo + 1);
+                if (P < W) {  // some warps own no page; count the live ones
+                    nseg = 0;
+                    for (int64_t s = wlo; s <= whi; ++s) nseg += warp_live(s, W, P);
+                }
+                if (prev == nseg - 1) {
+                    __threadfence();
+                    combine_item(p, item, wlo, whi, P, lane);
+                    if (lane == 0) p.item_sem[item] = 0;
                 }
             }
             if (x + 1 < x1) {
@@ -264,47 +388,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_kernel(const DecodeParam
                 len = p.item_len[item];
                 load_q();
             }
-        }
-    }
-}
-
-// K2: merge the partial slots of items split across warps (one warp/item).
-__global__ void __launch_bounds__(256) combine_kernel(const DecodeParams p) {
-    const int item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (item >= p.n_items) return;
-    const int64_t P = p.page_off[p.n_items];
-    const int64_t b = p.page_off[item], e = p.page_off[item + 1];
-    if (b == e) return;
-    const int64_t wlo = owner_warp(b, p.n_warps, P), whi = owner_warp(e - 1, p.n_warps, P);
-    if (wlo == whi) return;
-    const int64_t ob = (int64_t)p.item_orow[item] * p.qpk * kHeadDim;
-    for (int q = 0; q < p.qpk; ++q) {
-        float mx = -INFINITY;
-        for (int64_t s = wlo; s <= whi; ++s) mx = fmaxf(mx, p.part_lse[(item + s) * p.qpk + q]);
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        float den = 0.f;
-        for (int64_t s = wlo; s <= whi; ++s) {
-            const float wt = fast_exp2(p.part_lse[(item + s) * p.qpk + q] - mx);
-            const float4 v = reinterpret_cast<const float4 *>(
-                p.part_o + ((item + s) * p.qpk + q) * kHeadDim)[lane];
-            acc.x += wt * v.x;
-            acc.y += wt * v.y;
-            acc.z += wt * v.z;
-            acc.w += wt * v.w;
-            den += wt;
-        }
-        const float inv = 1.f / den;
-        if (p.out_fp32) {
-            reinterpret_cast<float4 *>(static_cast<float *>(p.out) + ob + q * kHeadDim)[lane] =
-                make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-        } else {
-            __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
-            __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
-            uint2 pk;
-            pk.x = *reinterpret_cast<uint32_t *>(&lo);
-            pk.y = *reinterpret_cast<uint32_t *>(&hi);
-            reinterpret_cast<uint2 *>(static_cast<__nv_bfloat16 *>(p.out) + ob + q * kHeadDim)[lane] = pk;
         }
     }
 }
@@ -333,39 +416,55 @@ __global__ void __launch_bounds__(1024) plan_pages_kernel(const int32_t *item_le
 }
 
 // ------------------------------------------------------------- configs ---
+// (warps per CTA, ring stages per warp, CTAs per SM); index = desc.config.
+// Pages in flight per SM = warps * stages * ctas (8 KiB each).
+#define FS_DECODE_CONFIGS(X) \
+    X(0, 4, 4, 1)            \
+    X(1, 4, 6, 1)            \
+    X(2, 8, 3, 1)            \
+    X(3, 8, 2, 1)            \
+    X(4, 2, 8, 1)            \
+    X(5, 4, 3, 1)            \
+    X(6, 4, 3, 2)            \
+    X(7, 2, 4, 3)
+
 struct KernelCfg {
-    int warps, stages;
+    int warps, stages, ctas;
 };
-// index = desc.config; 0 is the default
-static const KernelCfg kCfgs[] = {{4, 6}, {4, 4}, {8, 3}, {8, 2}, {2, 12}, {4, 8}};
+#define FS_CFG_ROW(i, w, s, c) {w, s, c},
+static const KernelCfg kCfgs[] = {FS_DECODE_CONFIGS(FS_CFG_ROW)};
+#undef FS_CFG_ROW
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 
-template <int WARPS, int STAGES>
-static int launch_decode(const DecodeParams &prm, int grid, cudaStream_t st) {
+template <int WARPS, int STAGES, int CTAS>
+static int launch_decode(const DecodeParams &prm, int sms, cudaStream_t st) {
     const size_t smem = (size_t)WARPS * STAGES * (kPageBytes + 8);
     static bool attr_set[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
     if (!attr_set[dev & 63]) {
-        FS_CUDA(cudaFuncSetAttribute(decode_kernel<WARPS, STAGES>,
+        FS_CUDA(cudaFuncSetAttribute(decode_kernel<WARPS, STAGES, CTAS>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set[dev & 63] = true;
     }
-    decode_kernel<WARPS, STAGES><<<grid, WARPS * 32, smem, st>>>(prm);
+    decode_kernel<WARPS, STAGES, CTAS><<<sms * CTAS, WARPS * 32, smem, st>>>(prm);
     return cuda_status(cudaGetLastError(), "decode_kernel launch");
 }
 
-static int warps_of(int config) { return kCfgs[config].warps; }
+static int warps_of(int config) { return kCfgs[config].warps * kCfgs[config].ctas; }
 
 }  // namespace fs
 
 using namespace fs;
 
 extern "C" int64_t fs_decode_partial_slots(int device, int32_t n_items, int32_t config) {
-    if (config < 0 || config >= kNumCfgs) return -1;
+    if (config < -1 || config >= kNumCfgs) return -1;
     const int sms = sm_count(device);
     if (sms <= 0) return -1;
-    return (int64_t)n_items + (int64_t)sms * warps_of(config);
+    int warps = 0;  // config -1: enough for every configuration
+    for (int c = 0; c < kNumCfgs; ++c)
+        if (config == -1 || c == config) warps = warps > warps_of(c) ? warps : warps_of(c);
+    return (int64_t)n_items + (int64_t)sms * warps;
 }
 
 extern "C" int fs_plan_pages(const int32_t *item_len, const int32_t *seg_items, int n_segs,
@@ -386,14 +485,16 @@ extern "C" int fs_decode_attention(const fs_decode_desc *d, void *stream) {
     FS_CHECK_ARG(d->config >= 0 && d->config < kNumCfgs, "unknown kernel config %d", d->config);
     if (d->n_items == 0) return FS_OK;
     FS_CHECK_ARG(d->q && d->kv_pool && d->block_table && d->item_seq && d->item_len &&
-                     d->item_qrow && d->item_orow && d->page_off && d->out && d->part_o &&
-                     d->part_lse,
+                     d->item_qoff && d->item_ooff && d->page_off && d->out && d->part_o &&
+                     d->part_lse && d->item_sem,
                  "null pointer in decode descriptor");
+    FS_CHECK_ARG(!d->kv_new || (d->item_koff && d->item_voff),
+                 "fused append needs item_koff and item_voff");
     FS_CHECK_ARG((reinterpret_cast<uintptr_t>(d->kv_pool) & 15) == 0, "kv_pool must be 16B aligned");
     const int sms = sm_count(d->device);
     if (sms <= 0) return fail(FS_ECUDA, "cannot query SM count of device %d", d->device);
     const KernelCfg cfg = kCfgs[d->config];
-    const int64_t W = (int64_t)sms * cfg.warps;
+    const int64_t W = (int64_t)sms * cfg.warps * cfg.ctas;
     FS_CHECK_ARG(d->partial_slots >= (int64_t)d->n_items + W,
                  "partial_slots %lld < required %lld", (long long)d->partial_slots,
                  (long long)(d->n_items + W));
@@ -404,9 +505,13 @@ extern "C" int fs_decode_attention(const fs_decode_desc *d, void *stream) {
     prm.bt_stride = d->bt_stride;
     prm.item_seq = d->item_seq;
     prm.item_len = d->item_len;
-    prm.item_qrow = d->item_qrow;
-    prm.item_orow = d->item_orow;
+    prm.item_qoff = d->item_qoff;
+    prm.item_ooff = d->item_ooff;
     prm.page_off = d->page_off;
+    prm.kv_new = static_cast<const __nv_bfloat16 *>(d->kv_new);
+    prm.item_koff = d->item_koff;
+    prm.item_voff = d->item_voff;
+    prm.item_sem = d->item_sem;
     prm.n_items = d->n_items;
     prm.qpk = d->q_per_kv;
     prm.scale_log2 = d->scale * 1.4426950408889634f;
@@ -416,17 +521,11 @@ extern "C" int fs_decode_attention(const fs_decode_desc *d, void *stream) {
     prm.part_lse = d->part_lse;
     prm.n_warps = W;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    int rc;
     switch (d->config) {
-        case 0: rc = launch_decode<4, 6>(prm, sms, st); break;
-        case 1: rc = launch_decode<4, 4>(prm, sms, st); break;
-        case 2: rc = launch_decode<8, 3>(prm, sms, st); break;
-        case 3: rc = launch_decode<8, 2>(prm, sms, st); break;
-        case 4: rc = launch_decode<2, 12>(prm, sms, st); break;
-        default: rc = launch_decode<4, 8>(prm, sms, st); break;
+#define FS_CFG_CASE(i, w, s, c) \
+    case i: return launch_decode<w, s, c>(prm, sms, st);
+        FS_DECODE_CONFIGS(FS_CFG_CASE)
+#undef FS_CFG_CASE
+        default: return fail(FS_EVALIDATION, "unknown kernel config %d", d->config);
     }
-    if (rc != FS_OK) return rc;
-    const int blocks = (d->n_items * 32 + 255) / 256;
-    combine_kernel<<<blocks, 256, 0, st>>>(prm);
-    return cuda_status(cudaGetLastError(), "combine_kernel launch");
 }

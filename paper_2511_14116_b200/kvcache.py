@@ -125,24 +125,41 @@ class PagedKVCache:
         dev = self.device
         self.pool = torch.empty((self.n_pages, N.PAGE_BYTES), dtype=torch.uint8, device=dev)
         self.block_table = torch.from_numpy(bt.astype(np.int32)).to(dev)
-        n_slots = work.n_slots
         self.item_seq = torch.arange(n_seq, dtype=torch.int32, device=dev)
         self.item_len = torch.zeros(n_seq, dtype=torch.int32, device=dev)
         self.item_pos = torch.zeros(n_seq, dtype=torch.int32, device=dev)
-        req = torch.from_numpy(work.item_req.astype(np.int64)).to(dev)
-        slot = torch.from_numpy(work.item_slot.astype(np.int64)).to(dev)
-        self.item_qrow = (req * n_slots + slot).to(torch.int32)
-        self.item_kvrow = (req * 2 * n_slots + slot).to(torch.int32)
+        self.item_sem = torch.zeros(n_seq, dtype=torch.int32, device=dev)
+        self._req = torch.from_numpy(work.item_req.astype(np.int64)).to(dev)
+        self._slot = torch.from_numpy(work.item_slot.astype(np.int64)).to(dev)
+        # default ("blocks") layout: the query / output block of item i is
+        # row request*n_slots + slot of a [B*n_slots, qpk, 128] tensor
+        row = self._req * work.n_slots + self._slot
+        self.item_qoff = (row * q_per_kv * N.HEAD_DIM).to(torch.int32)
+        self.item_ooff = self.item_qoff
+        self.fused = None  # (qoff, koff, voff) of the fused-qkv layout
         self.seg_items = torch.from_numpy(work.seg_items).to(dev)
         self.page_off = torch.zeros(n_seq + work.num_layers, dtype=torch.int32, device=dev)
         seg = work.seg_items
         self.max_items = int(max(seg[1:] - seg[:-1])) if work.num_layers else 0
-        slots = N.lib.fs_decode_partial_slots(self.dev_index, self.max_items, config)
+        slots = N.lib.fs_decode_partial_slots(self.dev_index, self.max_items, -1)
         if slots < 0:
             raise SimulationError(f"cannot size decode partials: {N.lib.fs_last_error()}")
         self.part_o = torch.empty((slots, q_per_kv, N.HEAD_DIM), dtype=torch.float32, device=dev)
         self.part_lse = torch.empty((slots, q_per_kv), dtype=torch.float32, device=dev)
-        self._desc = N.DecodeDesc()
+        self._descs = {}
+
+    def set_fused_layout(self) -> int:
+        """Use the fused projection layout: per request one row
+        ``[q slots (S*qpk*128) | k slots (S*128) | v slots (S*128)]``.
+        Returns the row width in elements."""
+        S, hd, qpk = self.work.n_slots, N.HEAD_DIM, self.qpk
+        rw = S * (qpk + 2) * hd
+        base = self._req * rw
+        self.fused = ((base + self._slot * qpk * hd).to(torch.int32),
+                      (base + S * qpk * hd + self._slot * hd).to(torch.int32),
+                      (base + S * (qpk + 1) * hd + self._slot * hd).to(torch.int32))
+        self._descs.clear()
+        return rw
 
     # ------------------------------------------------------------ lengths --
     def set_lengths(self, lens_per_request) -> None:
@@ -195,39 +212,32 @@ class PagedKVCache:
                                  N.HEAD_DIM, _stream()), "fs_kv_read")
         return k, v
 
-    def append_layer(self, layer: int, kv: torch.Tensor) -> None:
-        """K3 for one decode step: the new token of every item of ``layer``
-        (at position len-1) from the fused projection output
-        ``kv`` [B, 2*n_slots*128] bf16 (K slots then V slots)."""
-        a = int(self.work.seg_items[layer])
-        n = int(self.work.seg_items[layer + 1]) - a
-        if n == 0:
-            return
-        vptr = N.C.c_void_p(kv.data_ptr() + self.work.n_slots * N.HEAD_DIM * 2)
-        N.check(N.lib.fs_kv_write(N.ptr(self.pool), N.ptr(self.block_table), self.pages_per_seq,
-                                  _at(self.item_seq, a), _at(self.item_pos, a),
-                                  _at(self.item_kvrow, a), n, N.ptr(kv), vptr, N.HEAD_DIM,
-                                  _stream()), "fs_kv_write")
-
     # -------------------------------------------------------------- decode --
-    def decode_layer(self, layer: int, q: torch.Tensor, out: torch.Tensor,
-                     scale: float = None) -> None:
-        """K1+K2 for every item of ``layer``: q/out [B*n_slots, qpk, 128]
-        (out bf16 or fp32)."""
+    def _desc(self, layer, q, out, qkv, scale):
+        key = (layer, q.data_ptr(), out.data_ptr(), out.dtype, qkv, scale, self.config)
+        d = self._descs.get(key)
+        if d is not None:
+            return d
         a = int(self.work.seg_items[layer])
         n = int(self.work.seg_items[layer + 1]) - a
-        if n == 0:
-            return
-        d = self._desc
+        d = N.DecodeDesc()
         d.q = q.data_ptr()
         d.kv_pool = self.pool.data_ptr()
         d.block_table = self.block_table.data_ptr()
         d.bt_stride = self.pages_per_seq
         d.item_seq = _at(self.item_seq, a).value
         d.item_len = _at(self.item_len, a).value
-        d.item_qrow = _at(self.item_qrow, a).value
-        d.item_orow = d.item_qrow
+        if qkv:
+            qoff, koff, voff = self.fused
+            d.item_qoff = _at(qoff, a).value
+            d.kv_new = q.data_ptr()
+            d.item_koff = _at(koff, a).value
+            d.item_voff = _at(voff, a).value
+        else:
+            d.item_qoff = _at(self.item_qoff, a).value
+        d.item_ooff = _at(self.item_ooff, a).value
         d.page_off = _at(self.page_off, a + layer).value
+        d.item_sem = _at(self.item_sem, a).value
         d.n_items = n
         d.q_per_kv = self.qpk
         d.scale = (1.0 / math.sqrt(N.HEAD_DIM)) if scale is None else float(scale)
@@ -238,6 +248,30 @@ class PagedKVCache:
         d.partial_slots = self.part_o.shape[0]
         d.device = self.dev_index
         d.config = self.config
+        self._descs[key] = d
+        return d
+
+    def decode_layer(self, layer: int, q: torch.Tensor, out: torch.Tensor,
+                     scale: float = None) -> None:
+        """K1 (+ fused combine) for every item of ``layer``.  q / out are
+        [B*n_slots, qpk, 128] blocks (out bf16 or fp32); the KV must already
+        hold every token (see :meth:`write_tokens`)."""
+        if int(self.work.seg_items[layer + 1]) == int(self.work.seg_items[layer]):
+            return
+        d = self._desc(layer, q, out, False, scale)
+        N.check(N.lib.fs_decode_attention(N.C.byref(d), _stream()), "fs_decode_attention")
+
+    def decode_layer_fused(self, layer: int, qkv: torch.Tensor, out: torch.Tensor,
+                           scale: float = None) -> None:
+        """One decode step of ``layer`` from the fused projection output
+        ``qkv`` [B, row] (:meth:`set_fused_layout`): the new token's K/V are
+        appended into their pages inside the same launch (fused K3), then
+        attention over ``len`` tokens.  ``out`` is [B*n_slots, qpk, 128]."""
+        if self.fused is None:
+            raise ValidationError("call set_fused_layout() first")
+        if int(self.work.seg_items[layer + 1]) == int(self.work.seg_items[layer]):
+            return
+        d = self._desc(layer, qkv, out, True, scale)
         N.check(N.lib.fs_decode_attention(N.C.byref(d), _stream()), "fs_decode_attention")
 
     def layer_kv_bytes(self, layer: int) -> int:

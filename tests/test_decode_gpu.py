@@ -207,3 +207,157 @@ def test_decode_errors_map_to_reference_exceptions():
     with pytest.raises(ValidationError):
         cache.decode_layer(0, torch.zeros((1, 9, 128), dtype=torch.bfloat16, device="cuda"),
                            torch.zeros((1, 9, 128), dtype=torch.bfloat16, device="cuda"))
+
+
+def test_fused_append_then_decode():
+    """Fused K3: the token at len-1 comes from the projection row and is
+    both attended and persisted into its page by the decode launch."""
+    from oracle.attention import head_decode
+    from oracle.placement import owner_table
+    owner = owner_table("hybrid", 1, 8, range(3))
+    lens = [1, 16, 17, 40, 513, 2]
+    B = len(lens)
+    routing = {r: r % 3 for r in range(B)}
+    qpk = 4
+    work, cache = _build(owner, 1, routing, lens, qpk)
+    rw = cache.set_fused_layout()
+    gen = torch.Generator().manual_seed(11)
+    S = work.n_slots
+    kv = {}
+    seqs, poss, ks, vs = [], [], [], []
+    for i in range(work.n_items):
+        n = lens[work.item_req[i]]
+        k = _bf16(torch.randn((n, 128), generator=gen))
+        v = _bf16(torch.randn((n, 128), generator=gen))
+        kv[i] = (k, v)
+        if n > 1:
+            seqs.append(np.full(n - 1, i))
+            poss.append(np.arange(n - 1))
+            ks.append(k[:-1])
+            vs.append(v[:-1])
+    cache.write_tokens(np.concatenate(seqs), np.concatenate(poss), torch.cat(ks).cuda(),
+                       torch.cat(vs).cuda())
+    qkv = _bf16(torch.randn((B, rw), generator=gen))
+    for i in range(work.n_items):
+        r, j = work.item_req[i], work.item_slot[i]
+        qkv[r, S * qpk * 128 + j * 128:S * qpk * 128 + (j + 1) * 128] = kv[i][0][-1]
+        qkv[r, S * (qpk + 1) * 128 + j * 128:S * (qpk + 1) * 128 + (j + 1) * 128] = kv[i][1][-1]
+    out = torch.zeros((B * S, qpk, 128), dtype=torch.float32, device="cuda")
+    cache.decode_layer_fused(0, qkv.cuda(), out)
+    torch.cuda.synchronize()
+    exp = np.zeros(out.shape)
+    for i in range(work.n_items):
+        r, j = work.item_req[i], work.item_slot[i]
+        q = qkv[r, j * qpk * 128:(j + 1) * qpk * 128].view(qpk, 128).double().numpy()
+        k, v = kv[i]
+        exp[r * S + j] = head_decode(q, k.double().numpy(), v.double().numpy(), 1 / math.sqrt(128))
+    _close(out.cpu().numpy(), exp)
+    # the new token was persisted into its page
+    items = np.arange(work.n_items)
+    last = np.array([lens[work.item_req[i]] - 1 for i in items])
+    k2, v2 = cache.read_tokens(items, last)
+    for i in items:
+        assert torch.equal(k2[i].cpu(), kv[i][0][-1]) and torch.equal(v2[i].cpu(), kv[i][1][-1])
+    # semaphores are left zero for the next launch
+    assert int(cache.item_sem.abs().sum()) == 0
+
+
+def _tiny_model(L=2, H=8, qpk=4, hidden=256):
+    from paper_2511_14116_b200.core import ModelSpec
+    return ModelSpec(num_layers=L, num_kv_heads=H, num_q_heads=H * qpk, head_dim=128,
+                     hidden_dim=hidden, ffn_intermediate_dim=1024)
+
+
+def _engine_reference(model, x, kv_hist, lens, seed):
+    """torch fp32 reference of the hybrid decode step with bf16 rounding at
+    the same points as the engine (qkv, attention output, residual)."""
+    from paper_2511_14116_b200.hybrid import head_weights
+    x = x.float().cuda()
+    qpk, hd = model.q_heads_per_kv_head, 128
+    for layer in range(model.num_layers):
+        xb = x.to(torch.bfloat16)
+        acc = torch.zeros_like(x)
+        for h in range(model.num_kv_heads):
+            wq, wk, wv, wo = head_weights(model, layer, h, seed, "cuda")
+            q = (xb @ wq).float().view(-1, qpk, hd)
+            kn, vn = (xb @ wk), (xb @ wv)
+            outs = []
+            for r in range(x.shape[0]):
+                kp, vp = kv_hist[(layer, h, r)]
+                k = torch.cat([kp.cuda(), kn[r:r + 1]]).float()
+                v = torch.cat([vp.cuda(), vn[r:r + 1]]).float()
+                w = torch.softmax(q[r] @ k.T / math.sqrt(hd), dim=-1)
+                outs.append((w @ v).to(torch.bfloat16))
+            o = torch.stack(outs).view(x.shape[0], qpk * hd)
+            acc += (o @ wo).float()
+        x = (xb.float() + acc).to(torch.bfloat16).float()
+    return x
+
+
+def _engines(model, mode, world, lens, routing, seed, kv_hist):
+    from paper_2511_14116_b200.hybrid import HybridDecodeRank
+    from paper_2511_14116_b200.placement import make_placement, owner_array
+    plan = make_placement(mode, model, range(world))
+    owner = owner_array(plan, model.num_kv_heads)
+    ranks = []
+    for g in range(world):
+        e = HybridDecodeRank(model, owner, g, routing, len(lens), max(lens), seed=seed,
+                             page_order="shuffled")
+        e.set_lengths(lens)
+        w = e.work
+        seqs, poss, ks, vs = [], [], [], []
+        for i in range(w.n_items):
+            layer = int(np.searchsorted(w.seg_items, i, side="right") - 1)
+            kp, vp = kv_hist[(layer, int(w.item_head[i]), int(w.item_req[i]))]
+            if len(kp):
+                seqs.append(np.full(len(kp), i))
+                poss.append(np.arange(len(kp)))
+                ks.append(kp)
+                vs.append(vp)
+        e.cache.write_tokens(np.concatenate(seqs), np.concatenate(poss),
+                             torch.cat(ks).cuda(), torch.cat(vs).cuda())
+        ranks.append(e)
+    return ranks
+
+
+def test_engine_world_emulation_matches_single_gpu_and_reference():
+    """Decode form of parallel_forward: world 1 == emulated hybrid worlds
+    2/7 and cyclic 4 (ordered partial sums) == torch fp32 reference."""
+    from paper_2511_14116_b200.hybrid import emulated_parallel_step
+    model = _tiny_model()
+    lens = [5, 17, 1, 33, 16, 2]
+    B = len(lens)
+    gen = torch.Generator().manual_seed(2)
+    kv_hist = {}
+    for layer in range(model.num_layers):
+        for h in range(model.num_kv_heads):
+            for r in range(B):
+                kv_hist[(layer, h, r)] = (_bf16(torch.randn((lens[r] - 1, 128), generator=gen)),
+                                          _bf16(torch.randn((lens[r] - 1, 128), generator=gen)))
+    x0 = _bf16(torch.randn((B, model.hidden_dim), generator=gen))
+    ref = _engine_reference(model, x0, kv_hist, lens, seed=4)
+    one = _engines(model, "hybrid", 1, lens, {r: 0 for r in range(B)}, 4, kv_hist)[0]
+    y1 = one.step(x0.cuda()).float().clone()
+    err = float((y1 - ref).abs().max())
+    assert err <= 3e-2 * max(1.0, float(ref.abs().max())), err
+    for mode, world in (("hybrid", 2), ("hybrid", 7), ("cyclic", 4), ("hybrid", 5)):
+        routing = {r: (r * 3) % world for r in range(B)}
+        ranks = _engines(model, mode, world, lens, routing, 4, kv_hist)
+        yw = emulated_parallel_step(ranks, x0.cuda()).float()
+        err = float((yw - y1).abs().max())
+        assert err <= 3e-2 * max(1.0, float(y1.abs().max())), (mode, world, err)
+
+
+def test_engine_graph_capture_replays_identically():
+    model = _tiny_model(L=3)
+    lens = [40, 7, 64]
+    gen = torch.Generator().manual_seed(5)
+    kv_hist = {(l, h, r): (_bf16(torch.randn((lens[r] - 1, 128), generator=gen)),
+                           _bf16(torch.randn((lens[r] - 1, 128), generator=gen)))
+               for l in range(3) for h in range(8) for r in range(3)}
+    e = _engines(model, "hybrid", 1, lens, {0: 0, 1: 0, 2: 0}, 1, kv_hist)[0]
+    x0 = _bf16(torch.randn((3, model.hidden_dim), generator=gen)).cuda()
+    eager = e.step(x0).clone()
+    e.capture()
+    graphed = e.step(x0).clone()
+    assert torch.equal(eager, graphed)

@@ -13,8 +13,9 @@ ap.add_argument("--rank", type=int, default=0)
 ap.add_argument("--qpk", type=int, default=4)
 ap.add_argument("--batch", type=int, default=64)
 ap.add_argument("--ctx", type=int, default=4096)
-ap.add_argument("--configs", default="0,1,2,3,4,5")
+ap.add_argument("--configs", default="0,1,2,3,4,5,6,7")
 ap.add_argument("--iters", type=int, default=5)
+ap.add_argument("--graph", action="store_true")
 a = ap.parse_args()
 owner = np.array(owner_table("hybrid", a.layers, a.heads, range(a.world)), dtype=np.int32)
 routing = {r: r % a.world for r in range(a.batch)}
@@ -29,13 +30,23 @@ kvb = sum(cache.layer_kv_bytes(l) for l in range(a.layers))
 print(f"items={work.n_items} KV bytes/step={kvb/1e9:.3f} GB pages={cache.n_pages}")
 for cfg in [int(c) for c in a.configs.split(",")]:
     cache.config = cfg
-    for _ in range(2):
-        for l in range(a.layers): cache.decode_layer(l, q, out)
-    torch.cuda.synchronize()
+    try:
+        for _ in range(2):
+            for l in range(a.layers): cache.decode_layer(l, q, out)
+        torch.cuda.synchronize()
+    except Exception as exc:
+        print(f"config {cfg}: {exc}"); continue
+    run = lambda: [cache.decode_layer(l, q, out) for l in range(a.layers)]
+    if a.graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            run()
+        run = g.replay
+        run(); torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
     for _ in range(a.iters):
-        for l in range(a.layers): cache.decode_layer(l, q, out)
+        run()
     e.record(); torch.cuda.synchronize()
     ms = s.elapsed_time(e) / a.iters
     print(f"config {cfg}: {ms:.3f} ms/step  {kvb/ms/1e6:.1f} GB/s  ({kvb/ms/1e6/6543.4*100:.1f}% of 6543 GB/s)")
