@@ -166,13 +166,17 @@ int fs_kv_read(const void *kv_pool, const int32_t *block_table, int64_t bt_strid
                const int32_t *tok_dst, int32_t n_tok, void *k_dst, void *v_dst,
                int64_t dst_stride, void *stream);
 
-/* K5: dst[i] <- page page_ids[i] (dst may be mapped pinned host memory) */
+/* K5: backup gather.  Page page_ids[i] -> slot (dst_slots ? dst_slots[i] : i)
+ * of dst (FS_PAGE_BYTES per slot).  dst may be mapped pinned host memory:
+ * the copy then runs over PCIe from a single launch on a side stream. */
 int fs_pages_gather(const void *kv_pool, const int32_t *page_ids, int32_t n_pages,
-                    void *dst, int32_t max_ctas, void *stream);
+                    void *dst, const int32_t *dst_slots, int32_t max_ctas, void *stream);
 
-/* K6: page page_ids[i] <- src[i] (src may be mapped pinned host memory) */
+/* K6: restore scatter.  Slot (src_slots ? src_slots[i] : i) of src -> page
+ * page_ids[i].  src may be mapped pinned host memory (the KV backup). */
 int fs_pages_scatter(void *kv_pool, const int32_t *page_ids, int32_t n_pages,
-                     const void *src, int32_t max_ctas, void *stream);
+                     const void *src, const int32_t *src_slots, int32_t max_ctas,
+                     void *stream);
 
 /* K7: enable peer access (idempotent) and peer copy */
 int fs_enable_peer(int device, int peer);

@@ -62,10 +62,10 @@ _SIGS = {
     "fs_kv_read": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                              C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64,
                              C.c_void_p]),
-    "fs_pages_gather": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,
-                                  C.c_void_p]),
-    "fs_pages_scatter": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,
-                                   C.c_void_p]),
+    "fs_pages_gather": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                  C.c_int32, C.c_void_p]),
+    "fs_pages_scatter": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                   C.c_int32, C.c_void_p]),
     "fs_enable_peer": (C.c_int, [C.c_int, C.c_int]),
     "fs_copy_peer": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int64,
                                C.c_void_p]),

@@ -59,12 +59,18 @@ __device__ __forceinline__ bool warp_live(int64_t w, int64_t W, int64_t P) {
     return w * P / W < (w + 1) * P / W;
 }
 
-// largest i in [0, n) with off[i] <= x (off is nondecreasing, off[n] > x)
-__device__ __forceinline__ int find_item(const int32_t *off, int n, int64_t x) {
+// largest i in [0, n) with off[i] <= x (off is nondecreasing, off[n] > x):
+// a warp-cooperative 32-ary search (2 dependent rounds for <= 1024 items)
+__device__ __forceinline__ int find_item(const int32_t *off, int n, int64_t x, int lane) {
     int lo = 0, hi = n;  // invariant: off[lo] <= x < off[hi]
     while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (off[mid] <= x) lo = mid; else hi = mid;
+        const int step = (hi - lo + 31) >> 5;
+        const int cand = lo + lane * step;
+        const bool ok = cand < hi && off[cand] <= x;
+        const unsigned m = __ballot_sync(0xffffffffu, ok);
+        const int k = 31 - __clz(m);
+        lo += k * step;
+        hi = min(hi, lo + step);
     }
     return lo;
 }
@@ -116,19 +122,34 @@ __device__ __forceinline__ void combine_item(const DecodeParams &p, int item, in
         }
         const unsigned live_mask = __ballot_sync(0xffffffffu, ok);
         const int cnt = min(32, nseg - base);
-#pragma unroll 2
-        for (int j = 0; j < cnt; ++j) {
-            if (!((live_mask >> j) & 1u)) continue;  // warp-uniform
-            const float4 *blk = po + (int64_t)(base + j) * qpk * (kHeadDim / 4) + lane;
+        const int any_live = __ffs(live_mask) - 1;  // dead slots are never read
+        // two segments per round: all 2 x qpk float4 loads are issued before
+        // any is consumed, so a round costs one L2 round trip
+        for (int j = 0; j < cnt; j += 2) {
+            const int ja = ((live_mask >> j) & 1u) ? j : any_live;
+            const int jb = (j + 1 < cnt && ((live_mask >> (j + 1)) & 1u)) ? j + 1 : any_live;
+            const float4 *ba = po + (int64_t)(base + ja) * qpk * (kHeadDim / 4) + lane;
+            const float4 *bb = po + (int64_t)(base + jb) * qpk * (kHeadDim / 4) + lane;
+            float4 va[FS_MAX_Q_PER_KV], vb[FS_MAX_Q_PER_KV];
 #pragma unroll
             for (int q = 0; q < FS_MAX_Q_PER_KV; ++q) {
                 if (q < qpk) {
-                    const float w = __shfl_sync(0xffffffffu, wt[q], j);
-                    const float4 v = __ldcg(blk + q * (kHeadDim / 4));
-                    acc[q].x += w * v.x;
-                    acc[q].y += w * v.y;
-                    acc[q].z += w * v.z;
-                    acc[q].w += w * v.w;
+                    va[q] = __ldcg(ba + q * (kHeadDim / 4));
+                    vb[q] = __ldcg(bb + q * (kHeadDim / 4));
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < FS_MAX_Q_PER_KV; ++q) {
+                if (q < qpk) {
+                    // weights of dead / out-of-range segments are 0
+                    const float wa = __shfl_sync(0xffffffffu, wt[q], j);
+                    const float wb = __shfl_sync(0xffffffffu, j + 1 < 32 ? wt[q] : 0.f,
+                                                 (j + 1) & 31);
+                    const float wbb = (j + 1 < cnt) ? wb : 0.f;
+                    acc[q].x += wa * va[q].x + wbb * vb[q].x;
+                    acc[q].y += wa * va[q].y + wbb * vb[q].y;
+                    acc[q].z += wa * va[q].z + wbb * vb[q].z;
+                    acc[q].w += wa * va[q].w + wbb * vb[q].w;
                 }
             }
         }
@@ -178,23 +199,45 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) decode_kernel(const DecodePa
     __syncwarp();
 
     const int32_t *off = p.page_off;
-    const int first = find_item(off, p.n_items, x0);
+    const int first = find_item(off, p.n_items, x0, lane);
 
-    // ---- producer state (lane 0 only) ----
-    int pitem = first;
-    int64_t px = x0;
+    // ---- producer: lane-parallel page-id windows ----
+    // lane l holds the page id of page win+l (cur) and win+32+l (nxt); the
+    // block-table loads of a window are issued 32 pages before their use,
+    // so no global-load latency sits on the per-page critical path.
     const uint64_t pol = policy_evict_first();
-    auto issue = [&](int stage) {
-        while (px >= off[pitem + 1]) ++pitem;
-        const int64_t pg = p.bt[(int64_t)p.item_seq[pitem] * p.bt_stride + (px - off[pitem])];
-        const uint32_t bar = bar0 + 8 * stage;
-        mbar_expect_tx(bar, kPageBytes);
-        bulk_g2s(buf0 + stage * kPageBytes, p.kv + pg * kPageBytes, kPageBytes, bar, pol);
+    int64_t win = x0;
+    int wit = first;  // an item <= the item of page win (walk start)
+    auto window_ids = [&](int64_t base) -> int64_t {
+        const int64_t y = base + lane;
+        int it = wit;
+        int64_t pg = 0;
+        if (y < x1) {
+            while (y >= off[it + 1]) ++it;
+            pg = p.bt[(int64_t)p.item_seq[it] * p.bt_stride + (y - off[it])];
+        }
+        const int last = __shfl_sync(0xffffffffu, it, 31);
+        wit = max(wit, last);  // lanes past x1 kept `it` at the walk start
+        return pg;
+    };
+    int64_t cur_pg = window_ids(win);
+    int64_t nxt_pg = window_ids(win + 32);
+    int64_t px = x0;
+    auto issue = [&](int stage) {  // warp-uniform
+        if (px - win == 32) {
+            win += 32;
+            cur_pg = nxt_pg;
+            nxt_pg = window_ids(win + 32);
+        }
+        const int64_t pg = __shfl_sync(0xffffffffu, cur_pg, (int)(px - win));
+        if (lane == 0) {
+            const uint32_t bar = bar0 + 8 * stage;
+            mbar_expect_tx(bar, kPageBytes);
+            bulk_g2s(buf0 + stage * kPageBytes, p.kv + pg * kPageBytes, kPageBytes, bar, pol);
+        }
         ++px;
     };
-    if (lane == 0) {
-        for (int s = 0; s < STAGES && px < x1; ++s) issue(s);
-    }
+    for (int s = 0; s < STAGES && px < x1; ++s) issue(s);
 
     // ---- consumer state ----
     int item = first;
@@ -311,7 +354,7 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) decode_kernel(const DecodePa
             }
         }
         __syncwarp();
-        if (lane == 0 && px < x1) issue(stage);
+        if (px < x1) issue(stage);
         if (++stage == STAGES) {
             stage = 0;
             phase ^= 1u;

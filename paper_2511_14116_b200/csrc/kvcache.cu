@@ -52,11 +52,13 @@ __global__ void __launch_bounds__(256) kv_read_kernel(const uint8_t *pool, const
 // whole pages; 4 independent 16 B transfers per thread keep PCIe busy.
 template <bool GATHER>
 __global__ void __launch_bounds__(256) page_copy_kernel(uint8_t *pool, const int32_t *ids,
-                                                        int32_t n_pages, uint8_t *flat) {
+                                                        int32_t n_pages, uint8_t *flat,
+                                                        const int32_t *slots) {
     constexpr int kChunks = kPageBytes / 16;  // 512 per page
     for (int64_t pg = blockIdx.x; pg < n_pages; pg += gridDim.x) {
+        const int64_t slot = slots ? slots[pg] : pg;
         uint4 *pp = reinterpret_cast<uint4 *>(pool + (int64_t)ids[pg] * kPageBytes);
-        uint4 *fp = reinterpret_cast<uint4 *>(flat + pg * kPageBytes);
+        uint4 *fp = reinterpret_cast<uint4 *>(flat + slot * kPageBytes);
         uint4 v[kChunks / 256];
 #pragma unroll
         for (int j = 0; j < kChunks / 256; ++j)
@@ -108,7 +110,7 @@ extern "C" int fs_kv_read(const void *kv_pool, const int32_t *block_table, int64
 }
 
 static int page_copy(bool gather, void *pool, const int32_t *ids, int32_t n, void *flat,
-                     int32_t max_ctas, void *stream) {
+                     const int32_t *slots, int32_t max_ctas, void *stream) {
     FS_CHECK_ARG(n >= 0, "n_pages must be nonnegative");
     if (n == 0) return FS_OK;
     FS_CHECK_ARG(pool && ids && flat, "null pointer");
@@ -118,21 +120,25 @@ static int page_copy(bool gather, void *pool, const int32_t *ids, int32_t n, voi
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (gather)
         page_copy_kernel<true><<<grid, 256, 0, st>>>(static_cast<uint8_t *>(pool), ids, n,
-                                                     static_cast<uint8_t *>(flat));
+                                                     static_cast<uint8_t *>(flat), slots);
     else
         page_copy_kernel<false><<<grid, 256, 0, st>>>(static_cast<uint8_t *>(pool), ids, n,
-                                                      static_cast<uint8_t *>(flat));
+                                                      static_cast<uint8_t *>(flat), slots);
     return cuda_status(cudaGetLastError(), "page_copy_kernel launch");
 }
 
 extern "C" int fs_pages_gather(const void *kv_pool, const int32_t *page_ids, int32_t n_pages,
-                               void *dst, int32_t max_ctas, void *stream) {
-    return page_copy(true, const_cast<void *>(kv_pool), page_ids, n_pages, dst, max_ctas, stream);
+                               void *dst, const int32_t *dst_slots, int32_t max_ctas,
+                               void *stream) {
+    return page_copy(true, const_cast<void *>(kv_pool), page_ids, n_pages, dst, dst_slots,
+                     max_ctas, stream);
 }
 
 extern "C" int fs_pages_scatter(void *kv_pool, const int32_t *page_ids, int32_t n_pages,
-                                const void *src, int32_t max_ctas, void *stream) {
-    return page_copy(false, kv_pool, page_ids, n_pages, const_cast<void *>(src), max_ctas, stream);
+                                const void *src, const int32_t *src_slots, int32_t max_ctas,
+                                void *stream) {
+    return page_copy(false, kv_pool, page_ids, n_pages, const_cast<void *>(src), src_slots,
+                     max_ctas, stream);
 }
 
 extern "C" int fs_enable_peer(int device, int peer) {
