@@ -1,0 +1,258 @@
+"""Executing the backup / recovery plans on the GPU (K5, K6, K7).
+
+* :class:`KVBackupExecutor` turns the reference's host-backup watermarks
+  (``BackupState`` / ``advance_backup``, recovery.py:143-247) into
+  incremental page copies: every page whose tokens are all below a
+  request's watermark is gathered (``fs_pages_gather``, one launch) from the
+  rank's KV pool into a pinned host mirror on a low-priority side stream.
+  The watermark the executor reports back is page-aligned (a partially
+  filled page is copied once it is full), so the host copy is always exact.
+* :func:`restore_pages` executes ``pcie_host`` ``kv_slice`` transfers of
+  ``plan_kv_recovery`` (recovery.py:430-504): host mirror pages are
+  scattered into the new owner's pool (``fs_pages_scatter``, one launch).
+* :func:`copy_shards_p2p` executes weight transfers peer-to-peer over NVLink
+  (``fs_copy_peer``); the north star's "missing shards from surviving
+  peers" path (recovery.py:396-427 plans them as host loads).
+* :func:`recovery_microbench` -- BASELINE config 4 on one GPU.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .core import ValidationError
+
+
+def _stream_ptr(s):
+    return N.C.c_void_p(s.cuda_stream)
+
+
+class KVBackupExecutor:
+    """Incremental page backup of one rank's :class:`PagedKVCache`.
+
+    Host mirror slot == device page id (pinned, mapped), so a restore onto
+    the same layout is a plain scatter.  ``sync(watermarks)`` copies, for
+    every item of every request, the pages that became complete below the
+    request's token watermark since the last call.
+    """
+
+    def __init__(self, cache, max_ctas: int = 16):
+        self.cache = cache
+        self.host = torch.empty((cache.n_pages, N.PAGE_BYTES), dtype=torch.uint8,
+                                pin_memory=True)
+        self.stream = torch.cuda.Stream(device=cache.device, priority=0)
+        self.max_ctas = max_ctas
+        self.copied_pages = np.zeros(cache.work.n_items, dtype=np.int64)
+        self._bt = cache.block_table.cpu().numpy()
+        self.bytes_copied = 0
+
+    def pending_pages(self, watermarks) -> np.ndarray:
+        """Device page ids that become backed-up for per-request token
+        watermarks ``watermarks`` (array/mapping request -> tokens)."""
+        w = self.cache.work
+        marks = np.array([watermarks[int(r)] for r in w.item_req], dtype=np.int64) \
+            if w.n_items else np.zeros(0, np.int64)
+        full = marks // N.PAGE_TOKENS
+        ids = []
+        for i in np.flatnonzero(full > self.copied_pages):
+            ids.append(self._bt[i, self.copied_pages[i]:full[i]])
+            self.copied_pages[i] = full[i]
+        return np.concatenate(ids).astype(np.int32) if ids else np.zeros(0, np.int32)
+
+    def sync(self, watermarks) -> int:
+        """Launch the gather for newly backed pages on the side stream
+        (ordered after the current stream's work); returns pages copied."""
+        ids = self.pending_pages(watermarks)
+        if not len(ids):
+            return 0
+        cur = torch.cuda.current_stream(self.cache.device)
+        self.stream.wait_stream(cur)
+        with torch.cuda.stream(self.stream):
+            dev_ids = torch.from_numpy(ids).to(self.cache.device, non_blocking=True)
+            N.check(N.lib.fs_pages_gather(N.ptr(self.cache.pool), N.ptr(dev_ids), len(ids),
+                                          N.ptr(self.host), N.ptr(dev_ids), self.max_ctas,
+                                          _stream_ptr(self.stream)), "fs_pages_gather")
+            dev_ids.record_stream(self.stream)
+        self.bytes_copied += len(ids) * N.PAGE_BYTES
+        return len(ids)
+
+    def backed_tokens(self, request: int) -> int:
+        """Page-aligned tokens of ``request`` safely on the host (min over
+        the request's items on this rank)."""
+        w = self.cache.work
+        items = np.flatnonzero(w.item_req == request)
+        if not len(items):
+            return 0
+        return int(self.copied_pages[items].min()) * N.PAGE_TOKENS
+
+    def wait(self):
+        self.stream.synchronize()
+
+
+def restore_pages(pool: torch.Tensor, page_ids, host_src: torch.Tensor, src_slots,
+                  max_ctas: int = 0, stream=None) -> None:
+    """K6: pool[page_ids[i]] <- host_src[src_slots[i]] (one launch)."""
+    dev = pool.device
+    ids = torch.as_tensor(np.asarray(page_ids, dtype=np.int32)).to(dev)
+    slots = torch.as_tensor(np.asarray(src_slots, dtype=np.int32)).to(dev)
+    if ids.numel() != slots.numel():
+        raise ValidationError("page_ids and src_slots differ in length")
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    N.check(N.lib.fs_pages_scatter(N.ptr(pool), N.ptr(ids), ids.numel(), N.ptr(host_src),
+                                   N.ptr(slots), max_ctas, _stream_ptr(s)), "fs_pages_scatter")
+
+
+def copy_shards_p2p(dst: torch.Tensor, src: torch.Tensor, stream=None) -> None:
+    """K7: copy a weight-shard buffer from a surviving peer's HBM."""
+    if dst.numel() * dst.element_size() != src.numel() * src.element_size():
+        raise ValidationError("shard size mismatch")
+    dd, sd = dst.device.index, src.device.index
+    if dd != sd:
+        N.check(N.lib.fs_enable_peer(dd, sd), "fs_enable_peer")
+    s = stream if stream is not None else torch.cuda.current_stream(dst.device)
+    N.check(N.lib.fs_copy_peer(N.ptr(dst), dd, N.ptr(src), sd,
+                               dst.numel() * dst.element_size(), _stream_ptr(s)), "fs_copy_peer")
+
+
+# ---------------------------------------------------------------------------
+# BASELINE config 4 microbenchmark
+# ---------------------------------------------------------------------------
+
+PEER_GBS_REFERENCE = 770.0  # measured B200 NVLink peer copy (B200_PROFILING.md)
+
+
+def _time_ms(fn, reps=3):
+    fn()
+    torch.cuda.synchronize()
+    best = float("inf")
+    for _ in range(reps):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        torch.cuda.synchronize()
+        best = min(best, s.elapsed_time(e))
+    return best
+
+
+def recovery_microbench(batch: int = 64, ctx: int = 4096, fails=(7, 3, 5)) -> dict:
+    """Llama-3-70B, hybrid(8) -> on-demand shrink after 1-3 losses.
+
+    Per loss: the reference plans (plan_weight_recovery on_demand,
+    plan_kv_recovery host_restore with a fully backed-up host copy) give
+    the per-survivor byte counts; the heaviest survivor's KV restore is
+    executed with K6 from pinned host memory, its PCIe weight bytes with
+    an H2D copy, and the NVLink remainder with K7 when a peer GPU exists
+    (modeled at 770 GB/s on a one-GPU box).  Also measures the K5 backup
+    gather throughput and the per-decode-step backup volume."""
+    import os
+
+    from .core import load_config
+    from .placement import make_placement
+    from .recovery import BackupState, plan_kv_recovery, plan_weight_recovery
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    model = load_config(os.path.join(here, "data", "llama70b.toml"))[0]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    n_gpus = torch.cuda.device_count()
+    plan = make_placement("hybrid", model, range(8))
+    alive = list(range(8))
+    contexts = {r: ctx for r in range(batch)}
+    routing = {r: r % 8 for r in range(batch)}
+    backup = BackupState(host_memory_bytes=2 * 10 ** 12,
+                         kv_bytes_per_token=model.kv_bytes_per_token())
+    for r in range(batch):
+        backup.register(r)
+        backup.backed[r] = ctx
+    steps = []
+    max_bytes = 0
+    plans = []
+    for f in fails:
+        new_alive = [g for g in alive if g != f]
+        wp = plan_weight_recovery(model, plan, new_alive, "on_demand")
+        new_plan = wp.target_plan("hybrid", model)
+        new_routing = {r: new_alive[r % len(new_alive)] for r in range(batch)}
+        kp = plan_kv_recovery(backup, plan, new_plan, model, contexts, routing, new_routing,
+                              "host_restore")
+        kv_by = kp.pcie_bytes_by_gpu()
+        w_pcie, w_nvl = wp.pcie_bytes_by_gpu(), wp.nvlink_bytes_by_gpu()
+        g_kv = max(kv_by, key=kv_by.get)
+        g_w = max(w_pcie, key=w_pcie.get)
+        plans.append((f, len(new_alive), kv_by[g_kv], w_pcie[g_w], max(w_nvl.values()),
+                      kp.recompute_tokens))
+        max_bytes = max(max_bytes, kv_by[g_kv], w_pcie[g_w])
+        plan, alive, routing = new_plan, new_alive, new_routing
+
+    # pinned host source (the backup / host weight copy) and device targets
+    host = torch.empty(max_bytes, dtype=torch.uint8, pin_memory=True)
+    host.view(torch.int32).fill_(7)
+    dev_buf = torch.empty(max_bytes, dtype=torch.uint8, device=dev)
+    peer = None
+    if n_gpus > 1:
+        peer = torch.empty(max_bytes, dtype=torch.uint8, device=torch.device("cuda", 1))
+    for f, world, kv_bytes, w_pcie, w_nvl, recompute in plans:
+        n_pages = math.ceil(kv_bytes / N.PAGE_BYTES)
+        pool = dev_buf[: n_pages * N.PAGE_BYTES].view(n_pages, N.PAGE_BYTES)
+        ids = np.random.default_rng(f).permutation(n_pages).astype(np.int32)
+        slots = np.arange(n_pages, dtype=np.int32)
+        src = host[: n_pages * N.PAGE_BYTES]
+        zc_ms = _time_ms(lambda: restore_pages(pool, ids, src, slots))
+        # staged alternative: DMA the backup into the device (copy engine),
+        # then scatter device->device; the faster of the two is the path
+        stage = torch.empty_like(pool)
+        ids_d = torch.from_numpy(ids).to(dev)
+
+        def staged():
+            stage.view(-1).copy_(src, non_blocking=True)
+            N.check(N.lib.fs_pages_scatter(N.ptr(pool), N.ptr(ids_d), n_pages, N.ptr(stage),
+                                           None, 0, _stream_ptr(torch.cuda.current_stream())))
+        st_ms = _time_ms(staged)
+        del stage
+        kv_ms = min(zc_ms, st_ms)
+        w_ms = _time_ms(lambda: dev_buf[:w_pcie].copy_(host[:w_pcie], non_blocking=True))
+        if peer is not None:
+            p_ms = _time_ms(lambda: copy_shards_p2p(dev_buf[:w_nvl], peer[:w_nvl]))
+            p_kind = "measured (fs_copy_peer)"
+        else:
+            p_ms = w_nvl / (PEER_GBS_REFERENCE * 1e9) * 1e3
+            p_kind = "modeled at 770 GB/s (one-GPU box)"
+        # KV restore and weight loads share the survivor's PCIe link; the
+        # NVLink exchange overlaps them (recovery.py:511-525 ordering)
+        pcie_ms = kv_ms + w_ms
+        total = pcie_ms + max(0.0, p_ms - pcie_ms)
+        steps.append({"failed": f, "world_after": world,
+                      "kv_restore_bytes_max_gpu": kv_bytes, "kv_restore_ms": round(kv_ms, 3),
+                      "kv_restore_zero_copy_ms": round(zc_ms, 3),
+                      "kv_restore_staged_ms": round(st_ms, 3),
+                      "kv_restore_gbs": round(kv_bytes / kv_ms / 1e6, 1),
+                      "weight_pcie_bytes_max_gpu": w_pcie, "weight_h2d_ms": round(w_ms, 3),
+                      "weight_nvlink_bytes_max_gpu": w_nvl, "weight_p2p_ms": round(p_ms, 3),
+                      "weight_p2p_kind": p_kind, "recompute_requests": len(recompute),
+                      "recovery_ms": round(total, 3)})
+    # K5: backup gather throughput and per-step volume
+    n_bk = min(max_bytes // N.PAGE_BYTES, 131072)
+    pool = dev_buf[: n_bk * N.PAGE_BYTES].view(n_bk, N.PAGE_BYTES)
+    ids = torch.from_numpy(np.random.default_rng(0).permutation(n_bk).astype(np.int32)).to(dev)
+    hdst = host[: n_bk * N.PAGE_BYTES]
+
+    def gather():
+        N.check(N.lib.fs_pages_gather(N.ptr(pool), N.ptr(ids), n_bk, N.ptr(hdst), None, 0,
+                                      _stream_ptr(torch.cuda.current_stream())))
+    g_ms = _time_ms(gather)
+    new_pages_per_step = batch * model.num_layers * 1 / N.PAGE_TOKENS  # 1 TP head at N=8
+    del host, dev_buf, peer
+    torch.cuda.empty_cache()
+    return {"workload": "C4 Llama-3-70B, B=64, ctx 4096, hybrid(8); losses of GPU "
+                        + ", ".join(str(f) for f in fails) + " (on-demand weights + host KV restore)",
+            "steps": steps,
+            "target_ms": 1000.0,
+            "backup_gather_gbs": round(n_bk * N.PAGE_BYTES / g_ms / 1e6, 1),
+            "backup_pages_per_decode_step_n8": new_pages_per_step,
+            "backup_bytes_per_decode_step_n8": int(new_pages_per_step * N.PAGE_BYTES),
+            "note": "KV restore = K6 scatter from pinned host (PCIe); weights = reference "
+                    "on-demand plan bytes for the heaviest survivor"}
