@@ -435,6 +435,8 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) decode_kernel(const DecodePa
     }
 }
 
+#include "decode_cta.cuh"
+
 // K4: segmented exclusive prefix of pages per item (one CTA per segment).
 __global__ void __launch_bounds__(1024) plan_pages_kernel(const int32_t *item_len,
                                                           const int32_t *seg_items,
@@ -461,40 +463,51 @@ __global__ void __launch_bounds__(1024) plan_pages_kernel(const int32_t *item_le
 // ------------------------------------------------------------- configs ---
 // (warps per CTA, ring stages per warp, CTAs per SM); index = desc.config.
 // Pages in flight per SM = warps * stages * ctas (8 KiB each).
+// kind 0: warp-level stream-K (decode_kernel); kind 1: CTA-level stream-K
+// (decode_cta_kernel, per-CTA smem merge).
 #define FS_DECODE_CONFIGS(X) \
-    X(0, 4, 4, 1)            \
-    X(1, 4, 6, 1)            \
-    X(2, 8, 3, 1)            \
-    X(3, 8, 2, 1)            \
-    X(4, 2, 8, 1)            \
-    X(5, 4, 3, 1)            \
-    X(6, 4, 3, 2)            \
-    X(7, 2, 4, 3)
+    X(0, 8, 2, 1, 1)         \
+    X(1, 4, 4, 1, 1)         \
+    X(2, 8, 3, 1, 1)         \
+    X(3, 16, 1, 1, 1)        \
+    X(4, 12, 1, 1, 1)        \
+    X(5, 6, 2, 1, 1)         \
+    X(6, 4, 2, 2, 1)         \
+    X(7, 4, 4, 1, 0)         \
+    X(8, 4, 3, 1, 0)         \
+    X(9, 8, 2, 1, 0)         \
+    X(10, 2, 8, 1, 0)
 
 struct KernelCfg {
-    int warps, stages, ctas;
+    int warps, stages, ctas, kind;
 };
-#define FS_CFG_ROW(i, w, s, c) {w, s, c},
+#define FS_CFG_ROW(i, w, s, c, k) {w, s, c, k},
 static const KernelCfg kCfgs[] = {FS_DECODE_CONFIGS(FS_CFG_ROW)};
 #undef FS_CFG_ROW
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 
-template <int WARPS, int STAGES, int CTAS>
+template <int WARPS, int STAGES, int CTAS, int KIND>
 static int launch_decode(const DecodeParams &prm, int sms, cudaStream_t st) {
-    const size_t smem = (size_t)WARPS * STAGES * (kPageBytes + 8);
+    size_t smem = (size_t)WARPS * STAGES * (kPageBytes + 8);
+    if (KIND == 1)
+        smem += (size_t)WARPS * (2 * FS_MAX_Q_PER_KV + FS_MAX_Q_PER_KV * kMergeStride) * 4;
     static bool attr_set[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
+    auto fn = KIND == 0 ? decode_kernel<WARPS, STAGES, CTAS> : decode_cta_kernel<WARPS, STAGES>;
     if (!attr_set[dev & 63]) {
-        FS_CUDA(cudaFuncSetAttribute(decode_kernel<WARPS, STAGES, CTAS>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set[dev & 63] = true;
     }
-    decode_kernel<WARPS, STAGES, CTAS><<<sms * CTAS, WARPS * 32, smem, st>>>(prm);
+    fn<<<sms * CTAS, WARPS * 32, smem, st>>>(prm);
     return cuda_status(cudaGetLastError(), "decode_kernel launch");
 }
 
-static int warps_of(int config) { return kCfgs[config].warps * kCfgs[config].ctas; }
+// stream-K partition units (warps for kind 0, CTAs for kind 1) per SM
+static int units_of(int config) {
+    const KernelCfg &k = kCfgs[config];
+    return k.kind == 0 ? k.warps * k.ctas : k.ctas;
+}
 
 }  // namespace fs
 
@@ -506,7 +519,7 @@ extern "C" int64_t fs_decode_partial_slots(int device, int32_t n_items, int32_t 
     if (sms <= 0) return -1;
     int warps = 0;  // config -1: enough for every configuration
     for (int c = 0; c < kNumCfgs; ++c)
-        if (config == -1 || c == config) warps = warps > warps_of(c) ? warps : warps_of(c);
+        if (config == -1 || c == config) warps = warps > units_of(c) ? warps : units_of(c);
     return (int64_t)n_items + (int64_t)sms * warps;
 }
 
@@ -537,7 +550,7 @@ extern "C" int fs_decode_attention(const fs_decode_desc *d, void *stream) {
     const int sms = sm_count(d->device);
     if (sms <= 0) return fail(FS_ECUDA, "cannot query SM count of device %d", d->device);
     const KernelCfg cfg = kCfgs[d->config];
-    const int64_t W = (int64_t)sms * cfg.warps * cfg.ctas;
+    const int64_t W = (int64_t)sms * units_of(d->config);
     FS_CHECK_ARG(d->partial_slots >= (int64_t)d->n_items + W,
                  "partial_slots %lld < required %lld", (long long)d->partial_slots,
                  (long long)(d->n_items + W));
@@ -565,8 +578,8 @@ extern "C" int fs_decode_attention(const fs_decode_desc *d, void *stream) {
     prm.n_warps = W;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (d->config) {
-#define FS_CFG_CASE(i, w, s, c) \
-    case i: return launch_decode<w, s, c>(prm, sms, st);
+#define FS_CFG_CASE(i, w, s, c, k) \
+    case i: return launch_decode<w, s, c, k>(prm, sms, st);
         FS_DECODE_CONFIGS(FS_CFG_CASE)
 #undef FS_CFG_CASE
         default: return fail(FS_EVALIDATION, "unknown kernel config %d", d->config);

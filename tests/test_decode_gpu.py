@@ -72,7 +72,7 @@ def _expected(work, kv, q, lens, n_rows):
 
 
 @pytest.mark.parametrize("qpk", [1, 4, 8])
-@pytest.mark.parametrize("config", [0, 2])
+@pytest.mark.parametrize("config", [0, 3, 7, 9])
 def test_decode_hybrid_rank_ragged(qpk, config):
     """Hybrid N=7 rank: 1 TP head for all requests + 1 DP head for routed
     requests; ragged lengths incl. 1, page edges and multi-warp items."""
@@ -209,7 +209,8 @@ def test_decode_errors_map_to_reference_exceptions():
                            torch.zeros((1, 9, 128), dtype=torch.bfloat16, device="cuda"))
 
 
-def test_fused_append_then_decode():
+@pytest.mark.parametrize("config", [0, 7])
+def test_fused_append_then_decode(config):
     """Fused K3: the token at len-1 comes from the projection row and is
     both attended and persisted into its page by the decode launch."""
     from oracle.attention import head_decode
@@ -219,7 +220,7 @@ def test_fused_append_then_decode():
     B = len(lens)
     routing = {r: r % 3 for r in range(B)}
     qpk = 4
-    work, cache = _build(owner, 1, routing, lens, qpk)
+    work, cache = _build(owner, 1, routing, lens, qpk, config=config)
     rw = cache.set_fused_layout()
     gen = torch.Generator().manual_seed(11)
     S = work.n_slots

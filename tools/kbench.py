@@ -13,7 +13,7 @@ ap.add_argument("--rank", type=int, default=0)
 ap.add_argument("--qpk", type=int, default=4)
 ap.add_argument("--batch", type=int, default=64)
 ap.add_argument("--ctx", type=int, default=4096)
-ap.add_argument("--configs", default="0,1,2,3,4,5,6,7")
+ap.add_argument("--configs", default="0,1,2,3,7")
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--graph", action="store_true")
 a = ap.parse_args()
