@@ -9,12 +9,13 @@ GPU; N>1 (torchrun, one process per GPU, NCCL) runs the same job split over
 N ranks (hybrid placement, least-loaded routing, NCCL all-reduce of the
 attention output).  One JSON line on rank 0.
 
-A *step* = one decode token for all 64 requests through every layer's
-attention sublayer: fused QKV GEMM (cuBLAS) -> ONE fs_decode_attention launch
-(KV append + paged GQA decode + split merge) -> output projection ->
-exchange (NCCL all-reduce when N>1) -> residual.  The whole step is one
-CUDA-graph replay.  The KV working set (34 GB at N=1) is far larger than L2,
-so no flush is needed between steps.
+A *step* = one decode token for all 64 requests through every layer:
+fused QKV GEMM (cuBLAS) -> ONE fs_decode_attention launch (KV append + paged
+GQA decode + split merge) -> output projection -> exchange (NCCL all-reduce
+when N>1) -> residual -> TP MLP partial over the rank's FFN shards (gate/up
+GEMM, fs_swiglu, down GEMM) -> exchange -> residual (``--no-mlp``: attention
+sublayer only).  The whole step is one CUDA-graph replay.  The KV working set
+(34 GB at N=1) is far larger than L2, so no flush is needed between steps.
 
 At N=1 the line also carries (rank 0 only):
 * ``failure_states`` -- BASELINE config 3 (Llama-3-70B-shaped, B=64,
@@ -128,11 +129,14 @@ def route(n_requests, ranks, ctx):
                                          output_len=1)) for i in range(n_requests)}
 
 
-def build_rank(model, owner, rank, routing, batch, ctx, group, config, seed=0):
+def build_rank(model, plan, rank, routing, batch, ctx, group, config, seed=0, mlp=True):
     import torch
     from paper_2511_14116_b200.hybrid import HybridDecodeRank
+    from paper_2511_14116_b200.placement import owner_array
+    owner = owner_array(plan, model.num_kv_heads)
+    shards = [plan.ffn.owner[s] for s in range(plan.ffn.num_shards)]
     eng = HybridDecodeRank(model, owner, rank, routing, batch, ctx, group=group, seed=seed,
-                           config=config)
+                           config=config, mlp=mlp, shard_owner=shards)
     eng.set_lengths([ctx] * batch)
     eng.fill_random_kv(seed + 17 * rank)
     eng.x.copy_(torch.randn_like(eng.x, dtype=torch.float32).to(torch.bfloat16))
@@ -183,7 +187,7 @@ def ncu_traffic():
 
 
 # ------------------------------------------------------- failure states --
-def failure_states(steps, warmup, config, batch=64, ctx=4096, fails=(7, 3, 5)):
+def failure_states(steps, warmup, config, batch=64, ctx=4096, fails=(7, 3, 5), mlp=True):
     import torch
     from paper_2511_14116_b200 import _native as N
     from paper_2511_14116_b200.placement import (make_placement, memory_footprint,
@@ -205,12 +209,15 @@ def failure_states(steps, warmup, config, batch=64, ctx=4096, fails=(7, 3, 5)):
         fp = memory_footprint(plan, model, {r: ctx for r in range(batch)}, routing)
         per_rank = []
         for g in alive:
-            eng = build_rank(model, owner, g, routing, batch, ctx, None, config)
+            eng = build_rank(model, plan, g, routing, batch, ctx, None, config, mlp=mlp)
             ms = time_graph(eng.step, min(steps, 20), warmup)
             kb = step_kv_bytes(eng)
             att = attention_op_graph(eng)
             att_ms = time_graph(att.replay, min(steps, 20), 2)
             per_rank.append({"rank": g, "step_ms": round(ms, 4), "kv_bytes": kb,
+                             "weight_bytes": eng.weight_bytes(),
+                             "step_frac": round((kb + eng.weight_bytes()) / (ms / 1e3) / 1e9 /
+                                                peak, 4),
                              "attn_ms": round(att_ms, 4),
                              "attn_gbs": round(kb / att_ms / 1e6, 1)})
             del eng, att
@@ -222,9 +229,11 @@ def failure_states(steps, warmup, config, batch=64, ctx=4096, fails=(7, 3, 5)):
             "max_kv_bytes": max(fp.values()),
             "kv_roofline_frac": round(max(fp.values()) / (worst["step_ms"] / 1e3) / 1e9 / peak, 4),
             "attn_frac_min": round(min(r["attn_gbs"] for r in per_rank) / peak, 4),
+            "step_frac_max_rank": worst["step_frac"],
             "ranks": per_rank})
     r8 = states[0]["tok_s"]
-    out = {"workload": "C3 Llama-3-70B-shaped attention, B=64, ctx 4096, hybrid(8) then "
+    out = {"workload": "C3 Llama-3-70B-shaped decode step (attention + TP MLP), B=64, "
+                       "ctx 4096, hybrid(8) then "
                        "on-demand shrink after failures of GPU 7, 3, 5",
            "emulation": "every rank of every world timed on this one GPU (graph replay); "
                         "step = max over ranks; the NCCL exchange is excluded (1 GPU)",
@@ -323,9 +332,10 @@ def run_reference(args, world, rank):
 
 
 def workload_config(model, world, batch, ctx):
-    return {"workload": "C2 Llama-3-8B-shaped hybrid-attention decode step "
-                        "(QKV GEMM, fused KV-append + paged GQA decode, O GEMM, "
-                        "NCCL all-reduce when N>1)",
+    return {"workload": "C2 Llama-3-8B-shaped hybrid-attention decode step, all 32 layers: "
+                        "QKV GEMM, fused KV-append + paged GQA decode, O GEMM, TP MLP "
+                        "partial (gate/up GEMM, swiglu, down GEMM); NCCL all-reduce of the "
+                        "attention and MLP partials when N>1",
             "layers": model.num_layers, "q_heads": model.num_q_heads,
             "kv_heads": model.num_kv_heads, "head_dim": model.head_dim,
             "hidden": model.hidden_dim, "batch": batch, "ctx": ctx, "world": world,
@@ -344,7 +354,8 @@ def run_ours(args, world, rank, local_rank):
     plan = make_placement("hybrid", model, range(world))
     owner = owner_array(plan, model.num_kv_heads)
     routing = route(batch, range(world), ctx)
-    eng = build_rank(model, owner, rank, routing, batch, ctx, group, args.kernel_config)
+    eng = build_rank(model, plan, rank, routing, batch, ctx, group, args.kernel_config,
+                     mlp=not args.no_mlp)
     peak, peak_src = measured_peaks()
 
     def barrier():
@@ -402,7 +413,9 @@ def run_ours(args, world, rank, local_rank):
                           "decode + in-kernel split merge), one launch per layer",
                 "bytes_per_launch": int(per_launch_bytes),
                 "launch_ms": round(per_launch_ms, 5), "peak_source": peak_src,
-                "step_kv_frac": round(kv_step / (ms / 1e3) / 1e9 / peak, 4)}
+                "step_kv_frac": round(kv_step / (ms / 1e3) / 1e9 / peak, 4),
+                "step_bytes": kv_step + eng.weight_bytes(),
+                "step_frac": round((kv_step + eng.weight_bytes()) / (ms / 1e3) / 1e9 / peak, 4)}
     del att
 
     line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
@@ -421,7 +434,8 @@ def run_ours(args, world, rank, local_rank):
 
     if world == 1 and rank == 0:
         if not args.skip_failure_states:
-            line["failure_states"] = failure_states(args.steps, args.warmup, args.kernel_config)
+            line["failure_states"] = failure_states(args.steps, args.warmup, args.kernel_config,
+                                                    mlp=not args.no_mlp)
         if not args.skip_recovery:
             try:
                 from paper_2511_14116_b200.recovery_exec import recovery_microbench
@@ -452,6 +466,8 @@ def main():
     ap.add_argument("--skip-failure-states", action="store_true")
     ap.add_argument("--skip-recovery", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--no-mlp", action="store_true",
+                    help="attention sublayer only (no TP MLP partial / MLP all-reduce)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     args = ap.parse_args()

@@ -178,6 +178,18 @@ int fs_pages_scatter(void *kv_pool, const int32_t *page_ids, int32_t n_pages,
                      const void *src, const int32_t *src_slots, int32_t max_ctas,
                      void *stream);
 
+/* TP MLP partial nonlinearity: out[r, c] = silu(h[r, c]) * h[r, cols + c]
+ * (bf16; h row stride ld >= 2*cols; gated FFN of core.py:93-95). */
+int fs_swiglu(const void *h, int64_t rows, int64_t cols, int64_t ld, void *out,
+              int64_t ld_out, void *stream);
+
+/* Synthetic weights: out[i, j] = scale * N(0,1) keyed by (seed, salt, global
+ * row, global col); global row = row_map ? row_map[i] : row_off + i (same for
+ * columns), so every rank materialises identical slices of one model. */
+int fs_fill_normal(void *out, int64_t rows, int64_t cols, int64_t ld,
+                   const int32_t *row_map, int64_t row_off, const int32_t *col_map,
+                   int64_t col_off, uint64_t seed, uint64_t salt, float scale, void *stream);
+
 /* K7: enable peer access (idempotent) and peer copy */
 int fs_enable_peer(int device, int peer);
 int fs_copy_peer(void *dst, int dst_device, const void *src, int src_device,

@@ -66,6 +66,11 @@ _SIGS = {
                                   C.c_int32, C.c_void_p]),
     "fs_pages_scatter": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                                    C.c_int32, C.c_void_p]),
+    "fs_swiglu": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int64,
+                            C.c_void_p]),
+    "fs_fill_normal": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
+                                 C.c_int64, C.c_void_p, C.c_int64, C.c_uint64, C.c_uint64,
+                                 C.c_float, C.c_void_p]),
     "fs_enable_peer": (C.c_int, [C.c_int, C.c_int]),
     "fs_copy_peer": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int64,
                                C.c_void_p]),
@@ -77,7 +82,7 @@ EXPORTS = tuple(_SIGS)
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_2511_14116_b200.build` "
+            f"{LIB_PATH} is missing: build it with `python paper_2511_14116_b200/build.py` "
             "(there is no CPU fallback)")
     lib = C.CDLL(LIB_PATH)
     for name, (res, args) in _SIGS.items():

@@ -1,6 +1,6 @@
 """Build libfailsafe_b200.so in-tree with nvcc for sm_100a (B200).
 
-    python -m paper_2511_14116_b200.build      # or __graft_entry__.build()
+    python paper_2511_14116_b200/build.py      # or __graft_entry__.build()
 
 The library is linked against the shared CUDA runtime (the libcudart.so.12
 torch already loaded), so streams created by torch are valid handles.
@@ -18,7 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libfailsafe_b200.so")
-SOURCES = ["abi.cpp", "planner.cpp", "decode.cu", "kvcache.cu"]
+SOURCES = ["abi.cpp", "planner.cpp", "decode.cu", "kvcache.cu", "mlp.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -549,7 +549,6 @@ extern "C" int fs_decode_attention(const fs_decode_desc *d, void *stream) {
     FS_CHECK_ARG((reinterpret_cast<uintptr_t>(d->kv_pool) & 15) == 0, "kv_pool must be 16B aligned");
     const int sms = sm_count(d->device);
     if (sms <= 0) return fail(FS_ECUDA, "cannot query SM count of device %d", d->device);
-    const KernelCfg cfg = kCfgs[d->config];
     const int64_t W = (int64_t)sms * units_of(d->config);
     FS_CHECK_ARG(d->partial_slots >= (int64_t)d->n_items + W,
                  "partial_slots %lld < required %lld", (long long)d->partial_slots,

@@ -9,18 +9,20 @@ For each layer, rank ``g``:
    work item into its page (fused K3) and attends every work item: TP
    slots for all requests, replicated slots only for requests routed to
    ``g`` (refexec.py:284-297), merging split items in-kernel (fused K2);
-4. ``part = o @ Wo_g`` -- rows of replicated slots for requests routed
-   elsewhere are zero, so their contribution is exactly zero
-   (refexec.py:290-297);
-5. the exchange: ``all_reduce(part)`` over the surviving ranks (NCCL over
-   NVLink; the reference's "exact sum in ascending rank order",
-   refexec.py:283-298), then ``x += part``.
+3. ``part = o @ Wo_g`` -- rows of replicated slots for requests routed
+   elsewhere are zero, so their contribution is exactly zero;
+4. exchange: ``all_reduce(part)`` over the surviving ranks (NCCL over
+   NVLink; the reference's exact sum in ascending rank order,
+   refexec.py:283-298), ``x += part``;
+5. (``mlp=True``) the TP MLP partial over the FFN shards the rank owns
+   (``plan.ffn``, refexec.py:299-307): ``act = swiglu(x @ [Wg|Wu]_g)``
+   (``fs_swiglu``), ``part = act @ Wd_g``, all-reduce, ``x += part``.
 
-Weights are derived per (layer, KV head) from a seed, so every rank of every
-world size builds bit-identical slices of one global model; the sum over
-ranks therefore reproduces the single-GPU result.  ``step`` can be captured
-into one CUDA graph (``capture=True``): a whole decode step is then a single
-graph launch.
+Weights are synthetic and keyed by GLOBAL (row, col) indices
+(``fs_fill_normal``): every rank of every world size -- including the
+on-demand targets after failures -- materialises bit-identical slices of one
+global model, so the sum over ranks reproduces the single-GPU result.
+``capture()`` records a whole step (all layers) as one CUDA graph.
 """
 
 from __future__ import annotations
@@ -34,39 +36,93 @@ from . import _native as N
 from .core import ModelSpec, ValidationError
 from .kvcache import PagedKVCache, RankWork
 
+# tensor ids of the synthetic weight salts
+_WQ, _WK, _WV, _WO, _WG, _WU, _WD = 1, 2, 3, 4, 5, 6, 7
+
+
+def _fill(out: torch.Tensor, layer: int, tensor: int, seed: int, scale: float,
+          row_off: int = 0, col_off: int = 0, col_map=None) -> None:
+    """Fill a 2-D bf16 (view) tensor with its slice of a global matrix."""
+    if out.dtype != torch.bfloat16 or out.dim() != 2 or out.stride(1) != 1:
+        raise ValidationError("fill target must be a row-major bf16 matrix")
+    cm = None
+    if col_map is not None:
+        cm = torch.as_tensor(np.asarray(col_map, dtype=np.int32)).to(out.device)
+    N.check(N.lib.fs_fill_normal(N.ptr(out), out.shape[0], out.shape[1], out.stride(0), None,
+                                 row_off, N.ptr(cm), col_off, seed, layer * 16 + tensor,
+                                 float(scale), N.C.c_void_p(
+                                     torch.cuda.current_stream(out.device).cuda_stream)),
+            "fs_fill_normal")
+
+
+def _scales(model: ModelSpec):
+    return (1.0 / math.sqrt(model.hidden_dim),
+            0.5 / math.sqrt(model.num_q_heads * model.head_dim),
+            0.5 / math.sqrt(model.ffn_intermediate_dim))
+
 
 def head_weights(model: ModelSpec, layer: int, head: int, seed: int, device):
-    """Deterministic weights of one KV head's group in one layer:
+    """The weights of KV head ``head``'s group in ``layer``:
     wq [hidden, qpk*hd], wk/wv [hidden, hd], wo [qpk*hd, hidden] (bf16)."""
     hd, qpk, hid = model.head_dim, model.q_heads_per_kv_head, model.hidden_dim
-    g = torch.Generator(device=device)
-    g.manual_seed((seed * 1_000_003 + layer * 4099 + head * 31) & 0x7FFFFFFF)
-    s_in = 1.0 / math.sqrt(hid)
-    s_out = 0.5 / math.sqrt(model.num_q_heads * hd)
-    wq = torch.randn((hid, qpk * hd), generator=g, device=device) * s_in
-    wk = torch.randn((hid, hd), generator=g, device=device) * s_in
-    wv = torch.randn((hid, hd), generator=g, device=device) * s_in
-    wo = torch.randn((qpk * hd, hid), generator=g, device=device) * s_out
-    return [w.to(torch.bfloat16) for w in (wq, wk, wv, wo)]
+    s_in, s_o, _ = _scales(model)
+    wq = torch.empty((hid, qpk * hd), dtype=torch.bfloat16, device=device)
+    wk = torch.empty((hid, hd), dtype=torch.bfloat16, device=device)
+    wv = torch.empty_like(wk)
+    wo = torch.empty((qpk * hd, hid), dtype=torch.bfloat16, device=device)
+    _fill(wq, layer, _WQ, seed, s_in, col_off=head * qpk * hd)
+    _fill(wk, layer, _WK, seed, s_in, col_off=head * hd)
+    _fill(wv, layer, _WV, seed, s_in, col_off=head * hd)
+    _fill(wo, layer, _WO, seed, s_o, row_off=head * qpk * hd)
+    return wq, wk, wv, wo
+
+
+def ffn_columns(model: ModelSpec, shard_owner, rank: int) -> np.ndarray:
+    """Global intermediate columns of the FFN shards ``rank`` owns
+    (ShardedView.shard_cols, refexec.py:150-154)."""
+    shards = [s for s, g in enumerate(shard_owner) if g == rank]
+    width = model.ffn_intermediate_dim // len(shard_owner)
+    return np.array([c for s in sorted(shards) for c in range(s * width, (s + 1) * width)],
+                    dtype=np.int32)
+
+
+def ffn_weights(model: ModelSpec, layer: int, cols, seed: int, device):
+    """wgu [hidden, 2*C] (gate | up columns), wd [C, hidden] for global
+    intermediate columns ``cols``."""
+    s_in, _, s_d = _scales(model)
+    C = len(cols)
+    hid = model.hidden_dim
+    wgu = torch.empty((hid, 2 * C), dtype=torch.bfloat16, device=device)
+    wd = torch.empty((C, hid), dtype=torch.bfloat16, device=device)
+    if C:
+        _fill(wgu[:, :C], layer, _WG, seed, s_in, col_map=cols)
+        _fill(wgu[:, C:], layer, _WU, seed, s_in, col_map=cols)
+        # down projection: generated as its transpose keyed (hidden, intermediate)
+        wdt = torch.empty((hid, C), dtype=torch.bfloat16, device=device)
+        _fill(wdt, layer, _WD, seed, s_d, col_map=cols)
+        wd.copy_(wdt.t())
+    return wgu, wd
 
 
 class HybridDecodeRank:
-    """One rank's share of the hybrid-attention decode step.
+    """One rank's share of the hybrid decode step.
 
-    ``owner``: int32 [L, H] table (``placement.owner_array``), ``routing``:
-    request -> GPU, ``group``: torch.distributed process group of the alive
-    ranks (None = no exchange, e.g. world 1 or single-GPU emulation).
+    ``owner``: int32 [L, H] (``placement.owner_array``); ``routing``:
+    request -> GPU; ``shard_owner``: FFN shard -> GPU (``plan.ffn``), needed
+    when ``mlp``; ``group``: torch.distributed group of the alive ranks
+    (None = no exchange: world 1 or single-GPU emulation).
     """
 
     def __init__(self, model: ModelSpec, owner, rank: int, routing, batch: int, capacity: int,
                  device=None, seed: int = 0, group=None, page_order: str = "contiguous",
-                 config: int = 0):
+                 config: int = 0, mlp: bool = False, shard_owner=None):
         if model.head_dim != N.HEAD_DIM:
             raise ValidationError(f"head_dim must be {N.HEAD_DIM} for the CUDA path")
         self.model = model
         self.rank = rank
         self.batch = batch
         self.group = group
+        self.mlp = mlp
         self.device = torch.device(device if device is not None else "cuda")
         self.qpk = model.q_heads_per_kv_head
         self.work = RankWork.build(np.asarray(owner, dtype=np.int32), rank, routing, batch)
@@ -78,20 +134,36 @@ class HybridDecodeRank:
         dev = self.device
         rw = self.cache.set_fused_layout()   # [q slots | k slots | v slots]
         qw = S * self.qpk * hd
+        s_in, s_o, _ = _scales(model)
         self.wqkv = torch.zeros((L, hid, rw), dtype=torch.bfloat16, device=dev)
         self.wo = torch.zeros((L, qw, hid), dtype=torch.bfloat16, device=dev)
         for layer in range(L):
             for j, h in enumerate(self.work.slot_heads[layer]):
-                wq, wk, wv, wo = head_weights(model, layer, h, seed, dev)
                 qs = slice(j * self.qpk * hd, (j + 1) * self.qpk * hd)
-                self.wqkv[layer, :, qs] = wq
-                self.wqkv[layer, :, qw + j * hd:qw + (j + 1) * hd] = wk
-                self.wqkv[layer, :, qw + (S + j) * hd:qw + (S + j + 1) * hd] = wv
-                self.wo[layer, qs, :] = wo
+                _fill(self.wqkv[layer, :, qs], layer, _WQ, seed, s_in, col_off=h * self.qpk * hd)
+                _fill(self.wqkv[layer, :, qw + j * hd:qw + (j + 1) * hd], layer, _WK, seed, s_in,
+                      col_off=h * hd)
+                _fill(self.wqkv[layer, :, qw + (S + j) * hd:qw + (S + j + 1) * hd], layer, _WV,
+                      seed, s_in, col_off=h * hd)
+                _fill(self.wo[layer, qs, :], layer, _WO, seed, s_o, row_off=h * self.qpk * hd)
         self.qkv = torch.empty((batch, rw), dtype=torch.bfloat16, device=dev)
         self.o = torch.zeros((batch * S, self.qpk, hd), dtype=torch.bfloat16, device=dev)
         self.part = torch.empty((batch, hid), dtype=torch.bfloat16, device=dev)
         self.x = torch.zeros((batch, hid), dtype=torch.bfloat16, device=dev)
+        self.ffn_cols = np.zeros(0, dtype=np.int32)
+        if mlp:
+            if shard_owner is None:
+                raise ValidationError("mlp=True needs the FFN shard owner table")
+            self.ffn_cols = ffn_columns(model, shard_owner, rank)
+            C = len(self.ffn_cols)
+            self.w_gu = torch.empty((L, hid, 2 * C), dtype=torch.bfloat16, device=dev)
+            self.w_d = torch.empty((L, C, hid), dtype=torch.bfloat16, device=dev)
+            for layer in range(L):
+                gu, d = ffn_weights(model, layer, self.ffn_cols, seed, dev)
+                self.w_gu[layer].copy_(gu)
+                self.w_d[layer].copy_(d)
+            self.h = torch.empty((batch, 2 * C), dtype=torch.bfloat16, device=dev)
+            self.act = torch.empty((batch, C), dtype=torch.bfloat16, device=dev)
         self._graph = None
 
     # ------------------------------------------------------------------ api --
@@ -106,12 +178,27 @@ class HybridDecodeRank:
         self.cache.pool.view(torch.bfloat16).normal_(generator=g)
 
     def attention_partial(self, layer: int) -> torch.Tensor:
-        """This rank's pre-exchange contribution of ``layer`` for the
-        current ``self.x``: ``o @ Wo_g`` [B, hidden] (into ``self.part``)."""
+        """This rank's pre-exchange attention contribution of ``layer`` for
+        the current ``self.x``: ``o @ Wo_g`` [B, hidden] (into ``self.part``)."""
         B, S, hd = self.batch, self.n_slots, self.model.head_dim
         torch.matmul(self.x, self.wqkv[layer], out=self.qkv)         # cuBLAS
         self.cache.decode_layer_fused(layer, self.qkv, self.o)       # K1 (+K2, +K3)
         torch.matmul(self.o.view(B, S * self.qpk * hd), self.wo[layer], out=self.part)
+        return self.part
+
+    def _swiglu(self) -> None:
+        C = self.act.shape[1]
+        N.check(N.lib.fs_swiglu(N.ptr(self.h), self.batch, C, 2 * C, N.ptr(self.act), C,
+                                N.C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)),
+                "fs_swiglu")
+
+    def mlp_partial(self, layer: int) -> torch.Tensor:
+        """This rank's pre-exchange MLP contribution (its FFN shards)."""
+        if not len(self.ffn_cols):
+            return self.part.zero_()
+        torch.matmul(self.x, self.w_gu[layer], out=self.h)
+        self._swiglu()
+        torch.matmul(self.act, self.w_d[layer], out=self.part)
         return self.part
 
     def _layers(self) -> None:
@@ -122,14 +209,29 @@ class HybridDecodeRank:
                 torch.matmul(x, self.wqkv[layer], out=self.qkv)      # cuBLAS
                 self.cache.decode_layer_fused(layer, self.qkv, self.o)
                 x.addmm_(o2, self.wo[layer])                         # x += o Wo
+                if self.mlp and len(self.ffn_cols):
+                    torch.matmul(x, self.w_gu[layer], out=self.h)
+                    self._swiglu()
+                    x.addmm_(self.act, self.w_d[layer])              # x += act Wd
             else:
                 self.attention_partial(layer)
                 torch.distributed.all_reduce(self.part, group=self.group)
                 x.add_(self.part)
+                if self.mlp:
+                    self.mlp_partial(layer)
+                    torch.distributed.all_reduce(self.part, group=self.group)
+                    x.add_(self.part)
 
     def launches_per_step(self) -> int:
-        """Our kernel launches per step: one fused decode launch per layer."""
-        return self.model.num_layers
+        """Our kernel launches per step: the fused decode launch per layer,
+        plus the swiglu launch per layer with the MLP."""
+        return self.model.num_layers * (2 if self.mlp and len(self.ffn_cols) else 1)
+
+    def weight_bytes(self) -> int:
+        n = self.wqkv.numel() + self.wo.numel()
+        if self.mlp:
+            n += self.w_gu.numel() + self.w_d.numel()
+        return 2 * n
 
     def capture(self) -> None:
         """Capture one decode step (all layers) into a CUDA graph."""
@@ -159,15 +261,18 @@ def emulated_parallel_step(ranks, x: torch.Tensor) -> torch.Tensor:
     """Single-process emulation of one hybrid decode step over several
     ranks (all on one GPU): per layer every rank computes its partial, the
     partials are summed in ascending rank order in fp32 (the reference's
-    ordered all-reduce, refexec.py:283-298) and the residual is applied.
-    Returns x after all layers."""
+    ordered all-reduce, refexec.py:283-298) and the residual is applied;
+    likewise for the MLP partials when the ranks carry the MLP."""
     ranks = sorted(ranks, key=lambda r: r.rank)
     x = x.to(torch.bfloat16)
     for layer in range(ranks[0].model.num_layers):
-        total = None
-        for r in ranks:
-            r.x.copy_(x)
-            part = r.attention_partial(layer).float()
-            total = part if total is None else total + part
-        x = x + total.to(torch.bfloat16)
+        for part_fn in ("attention_partial", "mlp_partial"):
+            if part_fn == "mlp_partial" and not ranks[0].mlp:
+                continue
+            total = None
+            for r in ranks:
+                r.x.copy_(x)
+                part = getattr(r, part_fn)(layer).float()
+                total = part if total is None else total + part
+            x = x + total.to(torch.bfloat16)
     return x

@@ -269,12 +269,13 @@ def _tiny_model(L=2, H=8, qpk=4, hidden=256):
                      hidden_dim=hidden, ffn_intermediate_dim=1024)
 
 
-def _engine_reference(model, x, kv_hist, lens, seed):
+def _engine_reference(model, x, kv_hist, lens, seed, mlp=False):
     """torch fp32 reference of the hybrid decode step with bf16 rounding at
-    the same points as the engine (qkv, attention output, residual)."""
-    from paper_2511_14116_b200.hybrid import head_weights
+    the same points as the engine (qkv, attention output, residual, MLP)."""
+    from paper_2511_14116_b200.hybrid import ffn_weights, head_weights
     x = x.float().cuda()
     qpk, hd = model.q_heads_per_kv_head, 128
+    all_cols = np.arange(model.ffn_intermediate_dim, dtype=np.int32)
     for layer in range(model.num_layers):
         xb = x.to(torch.bfloat16)
         acc = torch.zeros_like(x)
@@ -292,18 +293,27 @@ def _engine_reference(model, x, kv_hist, lens, seed):
             o = torch.stack(outs).view(x.shape[0], qpk * hd)
             acc += (o @ wo).float()
         x = (xb.float() + acc).to(torch.bfloat16).float()
+        if mlp:
+            xb = x.to(torch.bfloat16)
+            wgu, wd = ffn_weights(model, layer, all_cols, seed, "cuda")
+            C = len(all_cols)
+            hgu = (xb @ wgu).float()
+            act = (torch.nn.functional.silu(hgu[:, :C]) * hgu[:, C:]).to(torch.bfloat16)
+            x = (xb.float() + (act @ wd).float()).to(torch.bfloat16).float()
     return x
 
 
-def _engines(model, mode, world, lens, routing, seed, kv_hist):
+def _engines(model, mode, world, lens, routing, seed, kv_hist, mlp=False, plan=None):
     from paper_2511_14116_b200.hybrid import HybridDecodeRank
     from paper_2511_14116_b200.placement import make_placement, owner_array
-    plan = make_placement(mode, model, range(world))
+    if plan is None:
+        plan = make_placement(mode, model, range(world))
     owner = owner_array(plan, model.num_kv_heads)
+    shards = [plan.ffn.owner[s] for s in range(plan.ffn.num_shards)]
     ranks = []
-    for g in range(world):
+    for g in plan.alive:
         e = HybridDecodeRank(model, owner, g, routing, len(lens), max(lens), seed=seed,
-                             page_order="shuffled")
+                             page_order="shuffled", mlp=mlp, shard_owner=shards)
         e.set_lengths(lens)
         w = e.work
         seqs, poss, ks, vs = [], [], [], []
@@ -315,50 +325,80 @@ def _engines(model, mode, world, lens, routing, seed, kv_hist):
                 poss.append(np.arange(len(kp)))
                 ks.append(kp)
                 vs.append(vp)
-        e.cache.write_tokens(np.concatenate(seqs), np.concatenate(poss),
-                             torch.cat(ks).cuda(), torch.cat(vs).cuda())
+        if seqs:
+            e.cache.write_tokens(np.concatenate(seqs), np.concatenate(poss),
+                                 torch.cat(ks).cuda(), torch.cat(vs).cuda())
         ranks.append(e)
     return ranks
 
 
-def test_engine_world_emulation_matches_single_gpu_and_reference():
+def _history(model, lens, seed):
+    gen = torch.Generator().manual_seed(seed)
+    kv_hist = {}
+    for layer in range(model.num_layers):
+        for h in range(model.num_kv_heads):
+            for r in range(len(lens)):
+                kv_hist[(layer, h, r)] = (_bf16(torch.randn((lens[r] - 1, 128), generator=gen)),
+                                          _bf16(torch.randn((lens[r] - 1, 128), generator=gen)))
+    x0 = _bf16(torch.randn((len(lens), model.hidden_dim), generator=gen))
+    return kv_hist, x0
+
+
+@pytest.mark.parametrize("mlp", [False, True])
+def test_engine_world_emulation_matches_single_gpu_and_reference(mlp):
     """Decode form of parallel_forward: world 1 == emulated hybrid worlds
-    2/7 and cyclic 4 (ordered partial sums) == torch fp32 reference."""
+    2/7/5 and cyclic 4 (ordered partial sums) == torch fp32 reference."""
     from paper_2511_14116_b200.hybrid import emulated_parallel_step
     model = _tiny_model()
     lens = [5, 17, 1, 33, 16, 2]
     B = len(lens)
-    gen = torch.Generator().manual_seed(2)
-    kv_hist = {}
-    for layer in range(model.num_layers):
-        for h in range(model.num_kv_heads):
-            for r in range(B):
-                kv_hist[(layer, h, r)] = (_bf16(torch.randn((lens[r] - 1, 128), generator=gen)),
-                                          _bf16(torch.randn((lens[r] - 1, 128), generator=gen)))
-    x0 = _bf16(torch.randn((B, model.hidden_dim), generator=gen))
-    ref = _engine_reference(model, x0, kv_hist, lens, seed=4)
-    one = _engines(model, "hybrid", 1, lens, {r: 0 for r in range(B)}, 4, kv_hist)[0]
+    kv_hist, x0 = _history(model, lens, 2)
+    ref = _engine_reference(model, x0, kv_hist, lens, seed=4, mlp=mlp)
+    one = _engines(model, "hybrid", 1, lens, {r: 0 for r in range(B)}, 4, kv_hist, mlp=mlp)[0]
     y1 = one.step(x0.cuda()).float().clone()
     err = float((y1 - ref).abs().max())
     assert err <= 3e-2 * max(1.0, float(ref.abs().max())), err
     for mode, world in (("hybrid", 2), ("hybrid", 7), ("cyclic", 4), ("hybrid", 5)):
         routing = {r: (r * 3) % world for r in range(B)}
-        ranks = _engines(model, mode, world, lens, routing, 4, kv_hist)
+        ranks = _engines(model, mode, world, lens, routing, 4, kv_hist, mlp=mlp)
         yw = emulated_parallel_step(ranks, x0.cuda()).float()
         err = float((yw - y1).abs().max())
         assert err <= 3e-2 * max(1.0, float(y1.abs().max())), (mode, world, err)
 
 
+def test_engine_on_demand_targets_8_7_6_5_match_single_gpu():
+    """The failure states run the on-demand shrink targets (survivors keep
+    their heads/shards, lost heads replicated, lost shards redistributed):
+    each world's emulated step equals the single-GPU step."""
+    from paper_2511_14116_b200.hybrid import emulated_parallel_step
+    from paper_2511_14116_b200.placement import make_placement
+    from paper_2511_14116_b200.recovery import plan_weight_recovery
+    model = _tiny_model()
+    lens = [9, 33, 2, 17]
+    B = len(lens)
+    kv_hist, x0 = _history(model, lens, 8)
+    one = _engines(model, "hybrid", 1, lens, {r: 0 for r in range(B)}, 3, kv_hist, mlp=True)[0]
+    y1 = one.step(x0.cuda()).float().clone()
+    plan = make_placement("hybrid", model, range(8))
+    alive = list(range(8))
+    for f in (None, 7, 3, 5):
+        if f is not None:
+            alive = [g for g in alive if g != f]
+            plan = plan_weight_recovery(model, plan, alive, "on_demand").target_plan("hybrid",
+                                                                                      model)
+        routing = {r: alive[r % len(alive)] for r in range(B)}
+        ranks = _engines(model, "hybrid", None, lens, routing, 3, kv_hist, mlp=True, plan=plan)
+        yw = emulated_parallel_step(ranks, x0.cuda()).float()
+        err = float((yw - y1).abs().max())
+        assert err <= 3e-2 * max(1.0, float(y1.abs().max())), (f, err)
+
+
 def test_engine_graph_capture_replays_identically():
     model = _tiny_model(L=3)
     lens = [40, 7, 64]
-    gen = torch.Generator().manual_seed(5)
-    kv_hist = {(l, h, r): (_bf16(torch.randn((lens[r] - 1, 128), generator=gen)),
-                           _bf16(torch.randn((lens[r] - 1, 128), generator=gen)))
-               for l in range(3) for h in range(8) for r in range(3)}
-    e = _engines(model, "hybrid", 1, lens, {0: 0, 1: 0, 2: 0}, 1, kv_hist)[0]
-    x0 = _bf16(torch.randn((3, model.hidden_dim), generator=gen)).cuda()
-    eager = e.step(x0).clone()
+    kv_hist, x0 = _history(model, lens, 5)
+    e = _engines(model, "hybrid", 1, lens, {0: 0, 1: 0, 2: 0}, 1, kv_hist, mlp=True)[0]
+    eager = e.step(x0.cuda()).clone()
     e.capture()
-    graphed = e.step(x0).clone()
+    graphed = e.step(x0.cuda()).clone()
     assert torch.equal(eager, graphed)
