@@ -78,11 +78,23 @@ def _segments(n_tokens, seq_lens):
     return out
 
 
-def causal_head(lw, head, x, segs, rows=None):
-    """Causal attention of one (MHA) head restricted to ``rows``."""
+def bf16_round(a):
+    """Round to the nearest-even bfloat16 value (returned as float64): the
+    rounding the GPU path applies to q/K/V ("identical inputs")."""
+    f = np.asarray(a, dtype=np.float32)
+    u = f.view(np.uint32).astype(np.uint64)
+    u = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def causal_head(lw, head, x, segs, rows=None, qkv_round=None):
+    """Causal attention of one (MHA) head restricted to ``rows``;
+    ``qkv_round`` optionally rounds the projections (e.g. ``bf16_round``)."""
     q = x @ lw["wq"][head].T
     k = x @ lw["wk"][head].T
     v = x @ lw["wv"][head].T
+    if qkv_round is not None:
+        q, k, v = qkv_round(q), qkv_round(k), qkv_round(v)
     scale = 1.0 / np.sqrt(lw["wq"].shape[1])
     out = np.zeros_like(x)
     for s, e in segs:
@@ -110,7 +122,7 @@ def reference_forward(layers, x, seq_lens=None):
     return x
 
 
-def parallel_forward(layers, owner, shard_owner, alive, routing, x, seq_lens=None):
+def parallel_forward(layers, owner, shard_owner, alive, routing, x, seq_lens=None, qkv_round=None):
     """Hybrid forward on owner tables; ``routing`` maps request index ->
     GPU and only matters for replicated heads."""
     x = np.asarray(x, dtype=np.float64)
@@ -131,10 +143,10 @@ def parallel_forward(layers, owner, shard_owner, alive, routing, x, seq_lens=Non
         attn = np.zeros_like(x)
         for g in ranks:
             for h in sorted(h for h, o in enumerate(row) if o == g):
-                attn += causal_head(lw, h, x, segs)
+                attn += causal_head(lw, h, x, segs, qkv_round=qkv_round)
             if dp and rows_of[g].any():
                 for h in dp:
-                    attn += causal_head(lw, h, x, segs, rows=rows_of[g])
+                    attn += causal_head(lw, h, x, segs, rows=rows_of[g], qkv_round=qkv_round)
         x = x + attn
         ffn = np.zeros_like(x)
         for g in ranks:
