@@ -140,7 +140,8 @@ def build_rank(model, plan, rank, routing, batch, ctx, group, config, seed=0, ml
     eng.set_lengths([ctx] * batch)
     eng.fill_random_kv(seed + 17 * rank)
     eng.x.copy_(torch.randn_like(eng.x, dtype=torch.float32).to(torch.bfloat16))
-    eng.capture()
+    if os.environ.get("FS_BENCH_SHARED_GPU") != "1":  # gloo collectives are not capturable
+        eng.capture()
     return eng
 
 
@@ -406,7 +407,7 @@ def run_ours(args, world, rank, local_rank):
     per_launch_bytes = kv_step / model.num_layers
     per_launch_ms = att_ms / model.num_layers
     achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
-    traffic, _ = ncu_traffic()
+    traffic, _ = ncu_traffic() if world == 1 else (None, None)  # capture is of the N=1 config
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "kernel": "decode_kernel (fs_decode_attention: fused KV append + paged GQA "
@@ -482,11 +483,19 @@ def main():
     if args.impl == "reference":
         run_reference(args, world, rank)
         return
+    # FS_BENCH_SHARED_GPU=1 (testing only): every rank on cuda:0 with the gloo
+    # backend, to exercise the multi-rank path on a one-GPU box
+    shared = os.environ.get("FS_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local_rank = 0
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, world, rank, local_rank)
     finally:
