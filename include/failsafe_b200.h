@@ -178,6 +178,22 @@ int fs_pages_scatter(void *kv_pool, const int32_t *page_ids, int32_t n_pages,
                      const void *src, const int32_t *src_slots, int32_t max_ctas,
                      void *stream);
 
+/* Skinny weight-streaming GEMM of the decode step (tcgen05.mma + TMA,
+ * stream-K over (128-column tile, 64-k) units, persistent grid):
+ *   STORE    (0): out[n, c]  = sum_k x[n, k] W[k, c]
+ *   RESIDUAL (1): out[n, c]  = res[n, c] + sum_k x[n, k] W[k, c]  (out may == res)
+ *   SWIGLU   (2): out[n, 64t+j] = silu(g) * u with g, u the columns 128t+j and
+ *                 128t+64+j of x.W (gate/up interleaved in 64-column blocks)
+ * x: bf16 [rows <= 64][K] (row stride ld_x), W: bf16 [K][N] (row stride ld_w),
+ * K % 64 == 0, N % 128 == 0.  workspace: >= fs_gemm_workspace_floats fp32;
+ * sems: N/128 int32, zero-initialised (left zero).  Launched with
+ * programmatic dependent launch (W prefetch overlaps the previous kernel). */
+int64_t fs_gemm_workspace_floats(int device, int32_t N, int32_t epilogue);
+int fs_gemm_skinny(const void *x, int64_t ld_x, int32_t rows, int32_t K, const void *w,
+                   int64_t ld_w, int32_t N, void *out, int64_t ld_out, const void *res,
+                   int64_t ld_res, int32_t epilogue, float *workspace, int64_t ws_floats,
+                   int32_t *sems, int32_t device, void *stream);
+
 /* TP MLP partial nonlinearity: out[r, c] = silu(h[r, c]) * h[r, cols + c]
  * (bf16; h row stride ld >= 2*cols; gated FFN of core.py:93-95). */
 int fs_swiglu(const void *h, int64_t rows, int64_t cols, int64_t ld, void *out,

@@ -261,6 +261,7 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) decode_kernel(const DecodePa
 #pragma unroll
         for (int mt = 0; mt < 8; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
     };
+    grid_dependency_wait();  // q / kv_new come from the preceding GEMM
     load_q();
 
     int stage = 0;
@@ -499,7 +500,20 @@ static int launch_decode(const DecodeParams &prm, int sms, cudaStream_t st) {
         FS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set[dev & 63] = true;
     }
-    fn<<<sms * CTAS, WARPS * 32, smem, st>>>(prm);
+    // PDL: the prologue (table lookups, first TMA page loads) may overlap the
+    // tail of the preceding kernel; the kernel waits (griddepcontrol.wait)
+    // before its first read of q / kv_new and before any global write.
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(sms * CTAS);
+    lc.blockDim = dim3(WARPS * 32);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    FS_CUDA(cudaLaunchKernelEx(&lc, fn, prm));
     return cuda_status(cudaGetLastError(), "decode_kernel launch");
 }
 

@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_cta_kernel(const DecodeP
         ++px;
     };
     for (int s = 0; s < STAGES && px < n_my; ++s) issue(s);
+    grid_dependency_wait();  // q / kv_new come from the preceding GEMM
 
     // ---- consumer: items of the CTA range in order ----
     int item = first;

@@ -1,0 +1,483 @@
+// Skinny weight-streaming GEMM for the decode step on sm_100a:
+//     out[n, c] (+)= sum_k x[n, k] * W[k, c]        n < 64 (the decode batch)
+// computed as D^T[128 cols x 64 rows] = W^T-tile . x^T with tcgen05.mma
+// (M = 128 weight columns, N = 64 batch rows, K = 16 per instruction; A = the
+// W tile, MN-major, B = x, K-major, both TMA-loaded with 128B swizzle; the
+// fp32 accumulator lives in TMEM, double-buffered).
+//
+// Work decomposition is stream-K over (column tile, 64-wide k-step) units:
+// the persistent grid (one CTA per SM) splits the U = tiles x K/64 units
+// evenly, so skinny shapes with few column tiles (Llama-70B qkv at 8 GPUs:
+// 10 tiles) still use every SM and every byte of W is read exactly once.  A
+// CTA that covers a whole tile applies the epilogue directly; otherwise it
+// writes an fp32 partial to slot `tile + cta`, and the tile's last
+// contributor (semaphore) sums the partials in CTA order (deterministic).
+//
+// Roles (192 threads): warp 4 = TMA producer, warp 5 = MMA issuer, warps 0-3
+// = epilogue (TMEM lane quadrant = warp index).  Fused epilogues: plain
+// store, residual add (x += ...), and SwiGLU (tile = 64 gate + 64 up
+// columns -> 64 activations).  Launched with programmatic dependent launch:
+// W tiles of the first stages are fetched before griddepcontrol.wait, so the
+// weight stream starts while the previous kernel drains.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+
+namespace fs {
+
+constexpr int kGemmStages = 6;
+constexpr int kTileM = 128;        // weight columns per tile (UMMA M)
+constexpr int kRowsN = 64;         // batch rows (UMMA N)
+constexpr int kStepK = 64;         // k per stage (one 128B swizzle row)
+constexpr int kStageA = kTileM * kStepK * 2;   // 16 KB (two 64-col boxes)
+constexpr int kStageB = kRowsN * kStepK * 2;   // 8 KB
+constexpr int kStageBytes = kStageA + kStageB;
+constexpr int kStagePitch = kTileM + 4;        // fp32 staging row pitch (floats)
+constexpr int kGemmThreads = 192;
+
+enum GemmEpilogue { EPI_STORE = 0, EPI_RESIDUAL = 1, EPI_SWIGLU = 2 };
+
+struct GemmParams {
+    int32_t rows;       // valid batch rows (<= 64)
+    int32_t K;          // multiple of 64
+    int32_t tiles;      // output column tiles of 128
+    int64_t n_units;    // tiles * K/64
+    int32_t epilogue;
+    __nv_bfloat16 *out;
+    int64_t ld_out;
+    const __nv_bfloat16 *res;
+    int64_t ld_res;
+    float *ws;          // partial slots, each [64][128] fp32
+    int32_t *sems;      // per tile, zero-initialised, left zero
+};
+
+// ---------------------------------------------------------------- PTX ----
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int c0, int c1,
+                                            uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     bar)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                       uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// 32 lanes x 32 bit, 32 consecutive columns per thread
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_128B, Blackwell version 1
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;           // version
+    d |= (uint64_t)2 << 61;           // SWIZZLE_128B
+    return d;
+}
+
+// kind::f16 instruction descriptor: BF16 x BF16 -> F32, A MN-major, B K-major
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) |
+                            ((uint32_t)(kRowsN >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
+
+__device__ __forceinline__ int64_t gemm_owner(int64_t u, int64_t C, int64_t U) {
+    return ((u + 1) * C + U - 1) / U - 1;
+}
+__device__ __forceinline__ bool gemm_live(int64_t c, int64_t C, int64_t U) {
+    return c * U / C < (c + 1) * U / C;
+}
+
+__device__ __forceinline__ float silu(float g) { return g / (1.f + __expf(-g)); }
+
+// final epilogue from the fp32 staging tile stg[n][m] (128 epilogue threads)
+__device__ __forceinline__ void gemm_epilogue_store(const GemmParams &p, const float *stg, int tile,
+                                                    int tid) {
+    if (p.epilogue == EPI_SWIGLU) {
+        // 64 activations per row: silu(gate[j]) * up[j], j = m < 64
+        for (int i = tid; i < p.rows * 32; i += 128) {
+            const int n = i >> 5, j = (i & 31) * 2;
+            const float *row = stg + n * kStagePitch;
+            const float a0 = silu(row[j]) * row[64 + j];
+            const float a1 = silu(row[j + 1]) * row[64 + j + 1];
+            *reinterpret_cast<__nv_bfloat162 *>(p.out + n * p.ld_out + tile * 64 + j) =
+                __floats2bfloat162_rn(a0, a1);
+        }
+        return;
+    }
+    for (int i = tid; i < p.rows * 64; i += 128) {
+        const int n = i >> 6, m = (i & 63) * 2;
+        const float *row = stg + n * kStagePitch;
+        float a0 = row[m], a1 = row[m + 1];
+        const int64_t col = (int64_t)tile * kTileM + m;
+        if (p.epilogue == EPI_RESIDUAL) {
+            const float2 r = __bfloat1622float2(
+                *reinterpret_cast<const __nv_bfloat162 *>(p.res + n * p.ld_res + col));
+            a0 += r.x;
+            a1 += r.y;
+        }
+        *reinterpret_cast<__nv_bfloat162 *>(p.out + n * p.ld_out + col) = __floats2bfloat162_rn(a0, a1);
+    }
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_skinny_kernel(const __grid_constant__ CUtensorMap map_w,
+                       const __grid_constant__ CUtensorMap map_x, const GemmParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-byte aligned base for the swizzled stages
+    uint8_t *smem = reinterpret_cast<uint8_t *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t sbase = smem_u32(smem);
+    float *stg = reinterpret_cast<float *>(smem + kGemmStages * kStageBytes);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kGemmStages * kStageBytes +
+                                                  kRowsN * kStagePitch * 4);
+    const uint32_t bar_full = smem_u32(bars);
+    const uint32_t bar_empty = bar_full + 8 * kGemmStages;
+    const uint32_t bar_acc_full = bar_empty + 8 * kGemmStages;   // [2]
+    const uint32_t bar_acc_empty = bar_acc_full + 16;            // [2]
+    __shared__ uint32_t s_tmem;
+    __shared__ int s_prev;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t C = gridDim.x, U = p.n_units, c = blockIdx.x;
+    const int64_t u0 = c * U / C, u1 = (c + 1) * U / C;
+    const int nk = p.K / kStepK;
+
+    if (warp == 4 && lane == 0) {
+        prefetch_tmap(&map_w);
+        prefetch_tmap(&map_x);
+        for (int s = 0; s < kGemmStages; ++s) {
+            mbar_init(bar_full + 8 * s, 1);
+            mbar_init(bar_empty + 8 * s, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(bar_acc_full + 8 * b, 1);
+            mbar_init(bar_acc_empty + 8 * b, 128);
+        }
+        fence_barrier_init();
+        fence_proxy_async();
+    }
+    if (warp == 0) {  // TMEM: two 64-column fp32 accumulators
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&s_tmem)),
+                     "r"(128));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    if (u0 < u1) {
+        if (warp == 4) {
+            // ---------------- TMA producer ----------------
+            if (lane == 0) {
+                int stage = 0;
+                uint32_t phase = 0;
+                int issued = 0;
+                bool waited = false;
+                for (int64_t u = u0; u < u1; ++u) {
+                    const int t = (int)(u / nk), ks = (int)(u % nk);
+                    mbar_wait(bar_empty + 8 * stage, phase ^ 1u);
+                    const uint32_t a = sbase + stage * kStageBytes, b = a + kStageA;
+                    mbar_expect_tx(bar_full + 8 * stage, kStageBytes);
+                    tma_load_2d(a, &map_w, t * kTileM, ks * kStepK, bar_full + 8 * stage);
+                    tma_load_2d(a + kStageA / 2, &map_w, t * kTileM + 64, ks * kStepK,
+                                bar_full + 8 * stage);
+                    if (!waited && (++issued == kGemmStages || u + 1 == u1)) {
+                        // x comes from the preceding kernel: PDL wait, then
+                        // the B halves of every stage issued so far
+                        grid_dependency_wait();
+                        waited = true;
+                        int st = stage;
+                        for (int64_t v = u; v > u - issued; --v) {
+                            const int vks = (int)(v % nk);
+                            tma_load_2d(sbase + st * kStageBytes + kStageA, &map_x, vks * kStepK,
+                                        0, bar_full + 8 * st);
+                            st = st == 0 ? kGemmStages - 1 : st - 1;
+                        }
+                    } else if (waited) {
+                        tma_load_2d(b, &map_x, ks * kStepK, 0, bar_full + 8 * stage);
+                    }
+                    if (++stage == kGemmStages) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+                asm volatile("griddepcontrol.launch_dependents;");
+            }
+        } else if (warp == 5) {
+            // ---------------- MMA issuer ----------------
+            if (lane == 0) {
+                int stage = 0;
+                uint32_t phase = 0;
+                int seg = 0;
+                int64_t u = u0;
+                while (u < u1) {
+                    const int t = (int)(u / nk);
+                    const int64_t seg_end = min(u1, (int64_t)(t + 1) * nk);
+                    const int buf = seg & 1;
+                    mbar_wait(bar_acc_empty + 8 * buf, ((seg >> 1) & 1) ^ 1u);
+                    tc_fence_after();
+                    const uint32_t d = tmem + buf * kRowsN;
+                    bool first = true;
+                    for (; u < seg_end; ++u) {
+                        mbar_wait(bar_full + 8 * stage, phase);
+                        tc_fence_after();
+                        const uint32_t a = sbase + stage * kStageBytes, b = a + kStageA;
+#pragma unroll
+                        for (int j = 0; j < kStepK / 16; ++j) {
+                            const uint64_t ad = umma_desc(a + j * 2048, kStageA / 2, 1024);
+                            const uint64_t bd = umma_desc(b + j * 32, 16, 1024);
+                            tc_mma(d, ad, bd, kIdesc, first ? 0u : 1u);
+                            first = false;
+                        }
+                        tc_commit(bar_empty + 8 * stage);
+                        if (++stage == kGemmStages) {
+                            stage = 0;
+                            phase ^= 1u;
+                        }
+                    }
+                    tc_commit(bar_acc_full + 8 * buf);
+                    ++seg;
+                }
+            }
+        } else {
+            // ---------------- epilogue (warps 0-3) ----------------
+            const int tid = threadIdx.x;  // 0..127
+            const int m = warp * 32 + lane;
+            int seg = 0;
+            int64_t u = u0;
+            while (u < u1) {
+                const int t = (int)(u / nk);
+                const int64_t tb = (int64_t)t * nk, te = tb + nk;
+                const int64_t seg_end = min(u1, te);
+                const bool whole = u == tb && seg_end == te;
+                const int buf = seg & 1;
+                mbar_wait(bar_acc_full + 8 * buf, (seg >> 1) & 1);
+                tc_fence_after();
+                float acc[kRowsN];
+                {
+                    float v[32];
+                    const uint32_t taddr = tmem + buf * kRowsN + ((uint32_t)(warp * 32) << 16);
+                    tmem_ld32(taddr, v);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) acc[i] = v[i];
+                    tmem_ld32(taddr + 32, v);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) acc[32 + i] = v[i];
+                }
+                tc_fence_before();
+                mbar_arrive(bar_acc_empty + 8 * buf);
+                if (whole) {
+#pragma unroll
+                    for (int n = 0; n < kRowsN; ++n) stg[n * kStagePitch + m] = acc[n];
+                    named_bar_sync(2, 128);
+                    gemm_epilogue_store(p, stg, t, tid);
+                    named_bar_sync(2, 128);
+                } else {
+                    const int64_t slot = (int64_t)t + c;
+                    float *w = p.ws + slot * (kRowsN * kTileM);
+#pragma unroll
+                    for (int n = 0; n < kRowsN; ++n) __stcg(w + n * kTileM + m, acc[n]);
+                    __threadfence();
+                    named_bar_sync(2, 128);
+                    if (tid == 0) s_prev = atomicAdd(p.sems + t, 1);
+                    named_bar_sync(2, 128);
+                    const int64_t clo = gemm_owner(tb, C, U), chi = gemm_owner(te - 1, C, U);
+                    int nseg = (int)(chi - clo + 1);
+                    if (U < C) {
+                        nseg = 0;
+                        for (int64_t s = clo; s <= chi; ++s) nseg += gemm_live(s, C, U);
+                    }
+                    if (s_prev == nseg - 1) {
+                        __threadfence();
+                        // deterministic sum in CTA order into the staging tile
+                        for (int i = tid; i < kRowsN * kTileM / 4; i += 128) {
+                            float4 sacc = make_float4(0.f, 0.f, 0.f, 0.f);
+                            for (int64_t s = clo; s <= chi; ++s) {
+                                if (U < C && !gemm_live(s, C, U)) continue;
+                                const float4 v = __ldcg(reinterpret_cast<const float4 *>(
+                                                            p.ws + (t + s) * (kRowsN * kTileM)) +
+                                                        i);
+                                sacc.x += v.x;
+                                sacc.y += v.y;
+                                sacc.z += v.z;
+                                sacc.w += v.w;
+                            }
+                            const int n = (i * 4) / kTileM, mm = (i * 4) % kTileM;
+                            float *dst = stg + n * kStagePitch + mm;
+                            dst[0] = sacc.x;
+                            dst[1] = sacc.y;
+                            dst[2] = sacc.z;
+                            dst[3] = sacc.w;
+                        }
+                        named_bar_sync(2, 128);
+                        gemm_epilogue_store(p, stg, t, tid);
+                        if (tid == 0) p.sems[t] = 0;
+                    }
+                    named_bar_sync(2, 128);
+                }
+                u = seg_end;
+                ++seg;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
+    }
+}
+
+// ------------------------------------------------------------ host side ---
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// 2-D bf16 row-major [rows][cols] (row stride ld elements), box 64 x box_rows
+static int make_map(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
+                    int box_rows) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return fail(FS_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims,
+                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(FS_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return FS_OK;
+}
+
+static size_t gemm_smem() {
+    return 1024 + (size_t)kGemmStages * kStageBytes + (size_t)kRowsN * kStagePitch * 4 + 8 * 32;
+}
+
+}  // namespace fs
+
+using namespace fs;
+
+extern "C" int64_t fs_gemm_workspace_floats(int device, int32_t N, int32_t epilogue) {
+    const int sms = sm_count(device);
+    if (sms <= 0 || N <= 0) return -1;
+    const int64_t tiles = (int64_t)N / kTileM;
+    (void)epilogue;
+    return (tiles + sms) * (int64_t)kRowsN * kTileM;
+}
+
+extern "C" int fs_gemm_skinny(const void *x, int64_t ld_x, int32_t rows, int32_t K, const void *w,
+                              int64_t ld_w, int32_t N, void *out, int64_t ld_out, const void *res,
+                              int64_t ld_res, int32_t epilogue, float *workspace,
+                              int64_t ws_floats, int32_t *sems, int32_t device, void *stream) {
+    FS_CHECK_ARG(rows >= 1 && rows <= kRowsN, "rows must be in [1, %d], got %d", kRowsN, rows);
+    FS_CHECK_ARG(K > 0 && K % kStepK == 0, "K must be a positive multiple of %d", kStepK);
+    FS_CHECK_ARG(N > 0 && N % kTileM == 0, "N must be a positive multiple of %d", kTileM);
+    FS_CHECK_ARG(epilogue >= EPI_STORE && epilogue <= EPI_SWIGLU, "unknown epilogue %d", epilogue);
+    FS_CHECK_ARG(x && w && out && workspace && sems, "null pointer");
+    FS_CHECK_ARG(epilogue != EPI_RESIDUAL || res, "residual epilogue needs res");
+    FS_CHECK_ARG(ld_x % 8 == 0 && ld_w % 8 == 0 && ld_x >= K && ld_w >= N,
+                 "leading dimensions must be multiples of 8 and cover the matrix");
+    const int sms = sm_count(device);
+    if (sms <= 0) return fail(FS_ECUDA, "cannot query SM count");
+    FS_CHECK_ARG(ws_floats >= fs_gemm_workspace_floats(device, N, epilogue), "workspace too small");
+    CUtensorMap mw, mx;
+    if (int rc = make_map(&mw, w, K, N, ld_w, kStepK)) return rc;
+    if (int rc = make_map(&mx, x, rows, K, ld_x, kRowsN)) return rc;
+    GemmParams prm;
+    prm.rows = rows;
+    prm.K = K;
+    prm.tiles = N / kTileM;
+    prm.n_units = (int64_t)prm.tiles * (K / kStepK);
+    prm.epilogue = epilogue;
+    prm.out = static_cast<__nv_bfloat16 *>(out);
+    prm.ld_out = ld_out;
+    prm.res = static_cast<const __nv_bfloat16 *>(res);
+    prm.ld_res = ld_res;
+    prm.ws = workspace;
+    prm.sems = sems;
+    const size_t smem = gemm_smem();
+    static bool attr_set[64] = {false};
+    if (!attr_set[device & 63]) {
+        FS_CUDA(cudaFuncSetAttribute(gemm_skinny_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        attr_set[device & 63] = true;
+    }
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(sms);
+    lc.blockDim = dim3(kGemmThreads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    FS_CUDA(cudaLaunchKernelEx(&lc, gemm_skinny_kernel, mw, mx, prm));
+    return FS_OK;
+}

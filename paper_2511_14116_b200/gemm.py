@@ -1,0 +1,73 @@
+"""Host side of the skinny tcgen05 GEMM (``fs_gemm_skinny``, csrc/gemm.cu).
+
+The decode step's four projections per layer run through it:
+
+* QKV      ``qkv = x @ Wqkv``                       (STORE)
+* O-proj   ``x  += o @ Wo``      world 1            (RESIDUAL, in place)
+           ``part = o @ Wo``     world > 1          (STORE, then all-reduce)
+* gate/up  ``act = silu(x@Wg) * (x@Wu)``            (SWIGLU, fused epilogue)
+* down     ``x  += act @ Wd`` / ``part = act @ Wd`` (RESIDUAL / STORE)
+
+Batches above 64 rows are processed in 64-row chunks.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _native as N
+from .core import ValidationError
+
+STORE, RESIDUAL, SWIGLU = 0, 1, 2
+MAX_ROWS = 64
+
+
+def interleave_gate_up(w_gate: torch.Tensor, w_up: torch.Tensor) -> torch.Tensor:
+    """[K, C] gate and up -> [K, 2C] with 64-column blocks g0 u0 g1 u1 ...
+    (the layout the SWIGLU epilogue expects; C % 64 == 0)."""
+    K, C = w_gate.shape
+    if C % 64:
+        raise ValidationError("gate/up width must be a multiple of 64")
+    g = w_gate.reshape(K, C // 64, 1, 64)
+    u = w_up.reshape(K, C // 64, 1, 64)
+    return torch.cat([g, u], dim=2).reshape(K, 2 * C).contiguous()
+
+
+class SkinnyGemm:
+    """Workspace + semaphores for ``fs_gemm_skinny`` on one device (shared
+    by all projections of an engine; launches are stream-ordered)."""
+
+    def __init__(self, max_n: int, device=None):
+        self.device = torch.device(device if device is not None else "cuda")
+        self.index = self.device.index if self.device.index is not None \
+            else torch.cuda.current_device()
+        floats = N.lib.fs_gemm_workspace_floats(self.index, max_n, 0)
+        if floats < 0:
+            raise ValidationError("cannot size the GEMM workspace")
+        self.max_n = max_n
+        self.ws = torch.empty(floats, dtype=torch.float32, device=self.device)
+        self.sems = torch.zeros(max(1, max_n // 128), dtype=torch.int32, device=self.device)
+
+    def __call__(self, x: torch.Tensor, w: torch.Tensor, out: torch.Tensor,
+                 epilogue: int = STORE, res: torch.Tensor = None) -> torch.Tensor:
+        if x.dtype != torch.bfloat16 or w.dtype != torch.bfloat16 or out.dtype != torch.bfloat16:
+            raise ValidationError("skinny GEMM operands must be bf16")
+        rows, K = x.shape
+        Kw, n = w.shape
+        if Kw != K or x.stride(1) != 1 or w.stride(1) != 1 or out.stride(1) != 1:
+            raise ValidationError("skinny GEMM: shape / layout mismatch")
+        if n > self.max_n:
+            raise ValidationError(f"N={n} exceeds the workspace sized for {self.max_n}")
+        if epilogue == RESIDUAL and res is None:
+            res = out
+        stream = N.C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        ws_floats = self.ws.numel()
+        for r0 in range(0, rows, MAX_ROWS):
+            r = min(MAX_ROWS, rows - r0)
+            xs, os = x[r0:r0 + r], out[r0:r0 + r]
+            rs = res[r0:r0 + r] if res is not None else None
+            N.check(N.lib.fs_gemm_skinny(
+                N.ptr(xs), x.stride(0), r, K, N.ptr(w), w.stride(0), n, N.ptr(os), out.stride(0),
+                N.ptr(rs), res.stride(0) if res is not None else 0, epilogue, N.ptr(self.ws),
+                ws_floats, N.ptr(self.sems), self.index, stream), "fs_gemm_skinny")
+        return out
