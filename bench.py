@@ -43,6 +43,7 @@ METRIC = ("decode tokens/s at 8→7→6→5 B200 (fraction of HBM roofline); "
           "failure recovery ms")
 UNIT = "tokens/s"
 KV_UNIT = 512  # bytes per (kv head, token): K+V, head_dim 128, bf16 (core.py:101-103)
+GEMM_BACKEND = "cublas"  # --gemm: projections via cuBLAS or the tcgen05 skinny GEMM
 
 
 def measured_peaks():
@@ -136,7 +137,7 @@ def build_rank(model, plan, rank, routing, batch, ctx, group, config, seed=0, ml
     owner = owner_array(plan, model.num_kv_heads)
     shards = [plan.ffn.owner[s] for s in range(plan.ffn.num_shards)]
     eng = HybridDecodeRank(model, owner, rank, routing, batch, ctx, group=group, seed=seed,
-                           config=config, mlp=mlp, shard_owner=shards)
+                           config=config, mlp=mlp, shard_owner=shards, gemm=GEMM_BACKEND)
     eng.set_lengths([ctx] * batch)
     eng.fill_random_kv(seed + 17 * rank)
     eng.x.copy_(torch.randn_like(eng.x, dtype=torch.float32).to(torch.bfloat16))
@@ -467,6 +468,7 @@ def main():
     ap.add_argument("--skip-failure-states", action="store_true")
     ap.add_argument("--skip-recovery", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--gemm", default="cublas", choices=("cublas", "tcgen05"))
     ap.add_argument("--no-mlp", action="store_true",
                     help="attention sublayer only (no TP MLP partial / MLP all-reduce)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
@@ -474,6 +476,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    global GEMM_BACKEND
+    GEMM_BACKEND = args.gemm
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -184,13 +184,15 @@ int fs_pages_scatter(void *kv_pool, const int32_t *page_ids, int32_t n_pages,
  *   RESIDUAL (1): out[n, c]  = res[n, c] + sum_k x[n, k] W[k, c]  (out may == res)
  *   SWIGLU   (2): out[n, 64t+j] = silu(g) * u with g, u the columns 128t+j and
  *                 128t+64+j of x.W (gate/up interleaved in 64-column blocks)
- * x: bf16 [rows <= 64][K] (row stride ld_x), W: bf16 [K][N] (row stride ld_w),
+ * x: bf16 [rows <= 64][K] (row stride ld_x), W: bf16 [K][N] (row stride ld_w,
+ * w_layout 0) or packed in 128-column panels [N/128][K][128] (w_layout 1:
+ * every 64 x 128 slice the kernel streams is one contiguous 16 KB block),
  * K % 64 == 0, N % 128 == 0.  workspace: >= fs_gemm_workspace_floats fp32;
- * sems: N/128 int32, zero-initialised (left zero).  Launched with
+ * sems: 2*N/128 int32, zero-initialised (left zero).  Launched with
  * programmatic dependent launch (W prefetch overlaps the previous kernel). */
 int64_t fs_gemm_workspace_floats(int device, int32_t N, int32_t epilogue);
 int fs_gemm_skinny(const void *x, int64_t ld_x, int32_t rows, int32_t K, const void *w,
-                   int64_t ld_w, int32_t N, void *out, int64_t ld_out, const void *res,
+                   int64_t ld_w, int32_t w_layout, int32_t N, void *out, int64_t ld_out, const void *res,
                    int64_t ld_res, int32_t epilogue, float *workspace, int64_t ws_floats,
                    int32_t *sems, int32_t device, void *stream);
 

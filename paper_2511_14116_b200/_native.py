@@ -68,7 +68,7 @@ _SIGS = {
                                    C.c_int32, C.c_void_p]),
     "fs_gemm_workspace_floats": (C.c_int64, [C.c_int, C.c_int32, C.c_int32]),
     "fs_gemm_skinny": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p,
-                                 C.c_int64, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p,
+                                 C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p,
                                  C.c_int64, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p,
                                  C.c_int32, C.c_void_p]),
     "fs_swiglu": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int64,

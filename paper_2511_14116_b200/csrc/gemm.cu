@@ -30,15 +30,16 @@
 
 namespace fs {
 
-constexpr int kGemmStages = 6;
+constexpr int kGemmStages = 8;
 constexpr int kTileM = 128;        // weight columns per tile (UMMA M)
 constexpr int kRowsN = 64;         // batch rows (UMMA N)
 constexpr int kStepK = 64;         // k per stage (one 128B swizzle row)
 constexpr int kStageA = kTileM * kStepK * 2;   // 16 KB (two 64-col boxes)
 constexpr int kStageB = kRowsN * kStepK * 2;   // 8 KB
 constexpr int kStageBytes = kStageA + kStageB;
-constexpr int kStagePitch = kTileM + 4;        // fp32 staging row pitch (floats)
+constexpr int kUpPitch = 64 + 4;              // fp32 row pitch of the swiglu 'up' stage
 constexpr int kGemmThreads = 192;
+constexpr int kPrefetchA = 3;   // W stages issued before the PDL wait
 
 enum GemmEpilogue { EPI_STORE = 0, EPI_RESIDUAL = 1, EPI_SWIGLU = 2 };
 
@@ -48,12 +49,15 @@ struct GemmParams {
     int32_t tiles;      // output column tiles of 128
     int64_t n_units;    // tiles * K/64
     int32_t epilogue;
+    int32_t w_packed;   // 1: W pre-packed in UMMA-canonical 16 KB blocks
+    const uint8_t *w_raw;
     __nv_bfloat16 *out;
     int64_t ld_out;
     const __nv_bfloat16 *res;
     int64_t ld_res;
     float *ws;          // partial slots, each [64][128] fp32
     int32_t *sems;      // per tile, zero-initialised, left zero
+    unsigned long long *dbg;  // optional per-CTA phase timestamps (ns)
 };
 
 // ---------------------------------------------------------------- PTX ----
@@ -114,14 +118,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// UMMA shared-memory descriptor, SWIZZLE_128B, Blackwell version 1
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// UMMA shared-memory descriptor (Blackwell version 1); layout 2 =
+// SWIZZLE_128B, 0 = no swizzle (canonical core-matrix interleave)
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                              uint32_t layout) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFF);
     d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
     d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
     d |= (uint64_t)1 << 46;           // version
-    d |= (uint64_t)2 << 61;           // SWIZZLE_128B
+    d |= (uint64_t)layout << 61;
     return d;
 }
 
@@ -136,35 +142,52 @@ __device__ __forceinline__ bool gemm_live(int64_t c, int64_t C, int64_t U) {
     return c * U / C < (c + 1) * U / C;
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ int ld_acquire(const int32_t *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ float silu(float g) { return g / (1.f + __expf(-g)); }
 
-// final epilogue from the fp32 staging tile stg[n][m] (128 epilogue threads)
-__device__ __forceinline__ void gemm_epilogue_store(const GemmParams &p, const float *stg, int tile,
-                                                    int tid) {
+// final epilogue straight from the accumulator registers: thread m owns
+// column m of the tile for all 64 rows, so for a fixed row a warp stores 32
+// consecutive bf16.  SwiGLU: warps 2-3 (the 'up' columns) stage through
+// shared memory, warps 0-1 (gate) combine and store the 64 activations.
+__device__ __forceinline__ void gemm_epilogue(const GemmParams &p, const float (&acc)[kRowsN],
+                                              int tile, int m, float *up) {
     if (p.epilogue == EPI_SWIGLU) {
-        // 64 activations per row: silu(gate[j]) * up[j], j = m < 64
-        for (int i = tid; i < p.rows * 32; i += 128) {
-            const int n = i >> 5, j = (i & 31) * 2;
-            const float *row = stg + n * kStagePitch;
-            const float a0 = silu(row[j]) * row[64 + j];
-            const float a1 = silu(row[j + 1]) * row[64 + j + 1];
-            *reinterpret_cast<__nv_bfloat162 *>(p.out + n * p.ld_out + tile * 64 + j) =
-                __floats2bfloat162_rn(a0, a1);
+        if (m >= 64) {
+#pragma unroll
+            for (int n = 0; n < kRowsN; ++n) up[n * kUpPitch + (m - 64)] = acc[n];
+        }
+        named_bar_sync(2, 128);
+        if (m < 64) {
+#pragma unroll
+            for (int n = 0; n < kRowsN; ++n)
+                if (n < p.rows)
+                    p.out[n * p.ld_out + tile * 64 + m] =
+                        __float2bfloat16_rn(silu(acc[n]) * up[n * kUpPitch + m]);
         }
         return;
     }
-    for (int i = tid; i < p.rows * 64; i += 128) {
-        const int n = i >> 6, m = (i & 63) * 2;
-        const float *row = stg + n * kStagePitch;
-        float a0 = row[m], a1 = row[m + 1];
-        const int64_t col = (int64_t)tile * kTileM + m;
-        if (p.epilogue == EPI_RESIDUAL) {
-            const float2 r = __bfloat1622float2(
-                *reinterpret_cast<const __nv_bfloat162 *>(p.res + n * p.ld_res + col));
-            a0 += r.x;
-            a1 += r.y;
-        }
-        *reinterpret_cast<__nv_bfloat162 *>(p.out + n * p.ld_out + col) = __floats2bfloat162_rn(a0, a1);
+    const int64_t col = (int64_t)tile * kTileM + m;
+    if (p.epilogue == EPI_RESIDUAL) {
+#pragma unroll
+        for (int n = 0; n < kRowsN; ++n)
+            if (n < p.rows)
+                p.out[n * p.ld_out + col] =
+                    __float2bfloat16_rn(acc[n] + __bfloat162float(p.res[n * p.ld_res + col]));
+    } else {
+#pragma unroll
+        for (int n = 0; n < kRowsN; ++n)
+            if (n < p.rows) p.out[n * p.ld_out + col] = __float2bfloat16_rn(acc[n]);
     }
 }
 
@@ -176,15 +199,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint8_t *smem = reinterpret_cast<uint8_t *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = smem_u32(smem);
-    float *stg = reinterpret_cast<float *>(smem + kGemmStages * kStageBytes);
+    float *up = reinterpret_cast<float *>(smem + kGemmStages * kStageBytes);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kGemmStages * kStageBytes +
-                                                  kRowsN * kStagePitch * 4);
+                                                  kRowsN * kUpPitch * 4);
     const uint32_t bar_full = smem_u32(bars);
     const uint32_t bar_empty = bar_full + 8 * kGemmStages;
     const uint32_t bar_acc_full = bar_empty + 8 * kGemmStages;   // [2]
     const uint32_t bar_acc_empty = bar_acc_full + 16;            // [2]
+    const uint32_t bar_red = bar_acc_empty + 16;                 // split-tile gather
     __shared__ uint32_t s_tmem;
-    __shared__ int s_prev;
+
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t C = gridDim.x, U = p.n_units, c = blockIdx.x;
@@ -202,6 +226,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             mbar_init(bar_acc_full + 8 * b, 1);
             mbar_init(bar_acc_empty + 8 * b, 128);
         }
+        mbar_init(bar_red, 1);
         fence_barrier_init();
         fence_proxy_async();
     }
@@ -215,34 +240,43 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = s_tmem;
+    if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 8 + 0] = gtimer();
 
     if (u0 < u1) {
         if (warp == 4) {
             // ---------------- TMA producer ----------------
             if (lane == 0) {
+                const uint64_t pol = policy_evict_first();
                 int stage = 0;
                 uint32_t phase = 0;
                 int issued = 0;
                 bool waited = false;
-                for (int64_t u = u0; u < u1; ++u) {
-                    const int t = (int)(u / nk), ks = (int)(u % nk);
+                int t = (int)(u0 / nk), ks = (int)(u0 % nk);  // advanced incrementally
+                for (int64_t u = u0; u < u1; ++u, ks = (ks + 1 == nk) ? (++t, 0) : ks + 1) {
                     mbar_wait(bar_empty + 8 * stage, phase ^ 1u);
                     const uint32_t a = sbase + stage * kStageBytes, b = a + kStageA;
                     mbar_expect_tx(bar_full + 8 * stage, kStageBytes);
-                    tma_load_2d(a, &map_w, t * kTileM, ks * kStepK, bar_full + 8 * stage);
-                    tma_load_2d(a + kStageA / 2, &map_w, t * kTileM + 64, ks * kStepK,
-                                bar_full + 8 * stage);
-                    if (!waited && (++issued == kGemmStages || u + 1 == u1)) {
+                    if (p.w_packed) {  // one contiguous 16 KB block, one bulk copy
+                        bulk_g2s(a, p.w_raw + ((int64_t)t * nk + ks) * kStageA, kStageA,
+                                 bar_full + 8 * stage, pol);
+                    } else {
+                        tma_load_2d(a, &map_w, t * kTileM, ks * kStepK, bar_full + 8 * stage);
+                        tma_load_2d(a + kStageA / 2, &map_w, t * kTileM + 64, ks * kStepK,
+                                    bar_full + 8 * stage);
+                    }
+                    if (!waited && (++issued == kPrefetchA || u + 1 == u1)) {
                         // x comes from the preceding kernel: PDL wait, then
                         // the B halves of every stage issued so far
+                        if (p.dbg) p.dbg[blockIdx.x * 8 + 5] = gtimer();
                         grid_dependency_wait();
                         waited = true;
-                        int st = stage;
-                        for (int64_t v = u; v > u - issued; --v) {
-                            const int vks = (int)(v % nk);
+                        if (p.dbg) p.dbg[blockIdx.x * 8 + 6] = gtimer();
+                        int st = stage, vks = ks;
+                        for (int i = 0; i < issued; ++i) {
                             tma_load_2d(sbase + st * kStageBytes + kStageA, &map_x, vks * kStepK,
                                         0, bar_full + 8 * st);
                             st = st == 0 ? kGemmStages - 1 : st - 1;
+                            vks = vks == 0 ? nk - 1 : vks - 1;
                         }
                     } else if (waited) {
                         tma_load_2d(b, &map_x, ks * kStepK, 0, bar_full + 8 * stage);
@@ -271,12 +305,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     bool first = true;
                     for (; u < seg_end; ++u) {
                         mbar_wait(bar_full + 8 * stage, phase);
+                        if (p.dbg && u == u0) p.dbg[blockIdx.x * 8 + 1] = gtimer();
                         tc_fence_after();
                         const uint32_t a = sbase + stage * kStageBytes, b = a + kStageA;
 #pragma unroll
                         for (int j = 0; j < kStepK / 16; ++j) {
-                            const uint64_t ad = umma_desc(a + j * 2048, kStageA / 2, 1024);
-                            const uint64_t bd = umma_desc(b + j * 32, 16, 1024);
+                            // packed: no-swizzle canonical MN-major (k-group
+                            // stride 2048 B = LBO, m-group stride 128 B = SBO)
+                            const uint64_t ad = p.w_packed
+                                                    ? umma_desc(a + j * 4096, 2048, 128, 0)
+                                                    : umma_desc(a + j * 2048, kStageA / 2, 1024, 2);
+                            const uint64_t bd = umma_desc(b + j * 32, 16, 1024, 2);
                             tc_mma(d, ad, bd, kIdesc, first ? 0u : 1u);
                             first = false;
                         }
@@ -287,6 +326,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         }
                     }
                     tc_commit(bar_acc_full + 8 * buf);
+                    if (p.dbg) p.dbg[blockIdx.x * 8 + 2] = gtimer();
                     ++seg;
                 }
             }
@@ -296,6 +336,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const int m = warp * 32 + lane;
             int seg = 0;
             int64_t u = u0;
+            int pend[2], n_pend = 0;  // split tiles (only the range's first / last)
+            int n_red = 0;            // uses of bar_red (phase parity)
             while (u < u1) {
                 const int t = (int)(u / nk);
                 const int64_t tb = (int64_t)t * nk, te = tb + nk;
@@ -318,59 +360,95 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 tc_fence_before();
                 mbar_arrive(bar_acc_empty + 8 * buf);
                 if (whole) {
-#pragma unroll
-                    for (int n = 0; n < kRowsN; ++n) stg[n * kStagePitch + m] = acc[n];
-                    named_bar_sync(2, 128);
-                    gemm_epilogue_store(p, stg, t, tid);
-                    named_bar_sync(2, 128);
+                    gemm_epilogue(p, acc, t, m, up);
+                    named_bar_sync(2, 128);  // 'up' staging reused by the next segment
                 } else {
+                    // split tile: publish this CTA's fp32 partial now (never
+                    // blocks); the reduction runs after every segment of this
+                    // CTA has been published, so no CTA waits on a chain
                     const int64_t slot = (int64_t)t + c;
-                    float *w = p.ws + slot * (kRowsN * kTileM);
+                    float *wsl = p.ws + slot * (kRowsN * kTileM);
 #pragma unroll
-                    for (int n = 0; n < kRowsN; ++n) __stcg(w + n * kTileM + m, acc[n]);
+                    for (int n = 0; n < kRowsN; ++n) __stcg(wsl + n * kTileM + m, acc[n]);
                     __threadfence();
                     named_bar_sync(2, 128);
-                    if (tid == 0) s_prev = atomicAdd(p.sems + t, 1);
-                    named_bar_sync(2, 128);
-                    const int64_t clo = gemm_owner(tb, C, U), chi = gemm_owner(te - 1, C, U);
-                    int nseg = (int)(chi - clo + 1);
-                    if (U < C) {
-                        nseg = 0;
-                        for (int64_t s = clo; s <= chi; ++s) nseg += gemm_live(s, C, U);
-                    }
-                    if (s_prev == nseg - 1) {
-                        __threadfence();
-                        // deterministic sum in CTA order into the staging tile
-                        for (int i = tid; i < kRowsN * kTileM / 4; i += 128) {
-                            float4 sacc = make_float4(0.f, 0.f, 0.f, 0.f);
-                            for (int64_t s = clo; s <= chi; ++s) {
-                                if (U < C && !gemm_live(s, C, U)) continue;
-                                const float4 v = __ldcg(reinterpret_cast<const float4 *>(
-                                                            p.ws + (t + s) * (kRowsN * kTileM)) +
-                                                        i);
-                                sacc.x += v.x;
-                                sacc.y += v.y;
-                                sacc.z += v.z;
-                                sacc.w += v.w;
-                            }
-                            const int n = (i * 4) / kTileM, mm = (i * 4) % kTileM;
-                            float *dst = stg + n * kStagePitch + mm;
-                            dst[0] = sacc.x;
-                            dst[1] = sacc.y;
-                            dst[2] = sacc.z;
-                            dst[3] = sacc.w;
-                        }
-                        named_bar_sync(2, 128);
-                        gemm_epilogue_store(p, stg, t, tid);
-                        if (tid == 0) p.sems[t] = 0;
-                    }
-                    named_bar_sync(2, 128);
+                    if (tid == 0) atomicAdd(p.sems + t, 1);
+                    if (n_pend < 2) pend[n_pend++] = t;
                 }
+                if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 8 + 3] = gtimer();
                 u = seg_end;
                 ++seg;
             }
+            // Split tiles: once every contributor published, contributor i
+            // reduces rows [64i/nseg, 64(i+1)/nseg) over all partials in CTA
+            // order (deterministic) and applies the epilogue; the last
+            // finisher resets the two per-tile counters.  Waits only target
+            // publications, which never block, so the grid cannot deadlock.
+            for (int k = 0; k < n_pend; ++k) {
+                const int t = pend[k];
+                const int64_t tb = (int64_t)t * nk, te = tb + nk;
+                int32_t *pub = p.sems + t, *fin = p.sems + p.tiles + t;
+                const int64_t clo = gemm_owner(tb, C, U), chi = gemm_owner(te - 1, C, U);
+                int nseg = 0, rank = 0;
+                for (int64_t s = clo; s <= chi; ++s) {
+                    const bool live = U >= C || gemm_live(s, C, U);
+                    nseg += live;
+                    rank += live && s < c;
+                }
+                const int r_lo = rank * kRowsN / nseg, r_hi = (rank + 1) * kRowsN / nseg;
+                const int R = min(r_hi, p.rows) - r_lo;
+                // the stage ring is idle now (every MMA of this CTA is done):
+                // one bulk copy per contributor pulls rows [r_lo, r_hi) of its
+                // partial, all in flight together -> one L2 round trip
+                float *red = reinterpret_cast<float *>(smem);
+                if (tid == 0) {
+                    while (ld_acquire(pub) < nseg) __nanosleep(32);
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    if (R > 0) {
+                        mbar_expect_tx(bar_red, (uint32_t)(nseg * R * kTileM * 4));
+                        int idx = 0;
+                        for (int64_t s = clo; s <= chi; ++s) {
+                            if (U < C && !gemm_live(s, C, U)) continue;
+                            bulk_g2s(sbase + idx * R * kTileM * 4,
+                                     p.ws + (t + s) * (kRowsN * kTileM) + r_lo * kTileM,
+                                     R * kTileM * 4, bar_red, policy_evict_first());
+                            ++idx;
+                        }
+                    }
+                }
+                if (R > 0) {
+                    mbar_wait(bar_red, (uint32_t)(n_red & 1));
+                    ++n_red;
+                    const bool swiglu = p.epilogue == EPI_SWIGLU;
+                    for (int r = 0; r < R; ++r) {
+                        const int n = r_lo + r;
+                        float g = 0.f, uu = 0.f;
+                        for (int idx = 0; idx < nseg; ++idx) {  // CTA order
+                            const float *row = red + (idx * R + r) * kTileM;
+                            g += row[m];
+                            if (swiglu && m < 64) uu += row[64 + m];
+                        }
+                        if (swiglu) {
+                            if (m < 64)
+                                p.out[n * p.ld_out + t * 64 + m] = __float2bfloat16_rn(silu(g) * uu);
+                        } else {
+                            const int64_t col = (int64_t)t * kTileM + m;
+                            if (p.epilogue == EPI_RESIDUAL)
+                                g += __bfloat162float(p.res[n * p.ld_res + col]);
+                            p.out[n * p.ld_out + col] = __float2bfloat16_rn(g);
+                        }
+                    }
+                }
+                named_bar_sync(2, 128);
+                if (tid == 0 && atomicAdd(fin, 1) == nseg - 1) {
+                    *pub = 0;
+                    *fin = 0;
+                }
+            }
+            if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 8 + 3] = gtimer();
         }
     }
+    if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 8 + 4] = gtimer();
     tc_fence_before();
     __syncthreads();
     if (warp == 0) {
@@ -415,24 +493,29 @@ static int make_map(CUtensorMap *map, const void *ptr, int64_t rows, int64_t col
     return FS_OK;
 }
 
+static unsigned long long *g_gemm_dbg = nullptr;  // fs_gemm_debug_timestamps
+
 static size_t gemm_smem() {
-    return 1024 + (size_t)kGemmStages * kStageBytes + (size_t)kRowsN * kStagePitch * 4 + 8 * 32;
+    return 1024 + (size_t)kGemmStages * kStageBytes + (size_t)kRowsN * kUpPitch * 4 + 8 * 40;
 }
 
 }  // namespace fs
 
 using namespace fs;
 
+// testing hook (not in the public header): per-CTA phase timestamps
+extern "C" void fs_gemm_debug_timestamps(unsigned long long *dev_buf) { g_gemm_dbg = dev_buf; }
+
 extern "C" int64_t fs_gemm_workspace_floats(int device, int32_t N, int32_t epilogue) {
     const int sms = sm_count(device);
     if (sms <= 0 || N <= 0) return -1;
     const int64_t tiles = (int64_t)N / kTileM;
     (void)epilogue;
-    return (tiles + sms) * (int64_t)kRowsN * kTileM;
+    return (tiles + sms) * (int64_t)kRowsN * kTileM;  // sems: 2 * tiles int32
 }
 
 extern "C" int fs_gemm_skinny(const void *x, int64_t ld_x, int32_t rows, int32_t K, const void *w,
-                              int64_t ld_w, int32_t N, void *out, int64_t ld_out, const void *res,
+                              int64_t ld_w, int32_t w_layout, int32_t N, void *out, int64_t ld_out, const void *res,
                               int64_t ld_res, int32_t epilogue, float *workspace,
                               int64_t ws_floats, int32_t *sems, int32_t device, void *stream) {
     FS_CHECK_ARG(rows >= 1 && rows <= kRowsN, "rows must be in [1, %d], got %d", kRowsN, rows);
@@ -441,20 +524,29 @@ extern "C" int fs_gemm_skinny(const void *x, int64_t ld_x, int32_t rows, int32_t
     FS_CHECK_ARG(epilogue >= EPI_STORE && epilogue <= EPI_SWIGLU, "unknown epilogue %d", epilogue);
     FS_CHECK_ARG(x && w && out && workspace && sems, "null pointer");
     FS_CHECK_ARG(epilogue != EPI_RESIDUAL || res, "residual epilogue needs res");
-    FS_CHECK_ARG(ld_x % 8 == 0 && ld_w % 8 == 0 && ld_x >= K && ld_w >= N,
+    FS_CHECK_ARG(ld_x % 8 == 0 && ld_w % 8 == 0 && ld_x >= K && (w_layout == 1 || ld_w >= N),
                  "leading dimensions must be multiples of 8 and cover the matrix");
     const int sms = sm_count(device);
     if (sms <= 0) return fail(FS_ECUDA, "cannot query SM count");
     FS_CHECK_ARG(ws_floats >= fs_gemm_workspace_floats(device, N, epilogue), "workspace too small");
     CUtensorMap mw, mx;
-    if (int rc = make_map(&mw, w, K, N, ld_w, kStepK)) return rc;
+    FS_CHECK_ARG(w_layout == 0 || w_layout == 1, "unknown W layout %d", w_layout);
     if (int rc = make_map(&mx, x, rows, K, ld_x, kRowsN)) return rc;
+    if (w_layout == 1) {
+        FS_CHECK_ARG((reinterpret_cast<uintptr_t>(w) & 15) == 0, "packed W must be 16B aligned");
+        mw = mx;  // unused: packed blocks are moved with 1-D bulk copies
+    } else {
+        if (int rc = make_map(&mw, w, K, N, ld_w, kStepK)) return rc;
+    }
     GemmParams prm;
     prm.rows = rows;
     prm.K = K;
     prm.tiles = N / kTileM;
     prm.n_units = (int64_t)prm.tiles * (K / kStepK);
     prm.epilogue = epilogue;
+    prm.w_packed = w_layout;
+    prm.w_raw = static_cast<const uint8_t *>(w);
+    prm.dbg = g_gemm_dbg;
     prm.out = static_cast<__nv_bfloat16 *>(out);
     prm.ld_out = ld_out;
     prm.res = static_cast<const __nv_bfloat16 *>(res);

@@ -33,6 +33,26 @@ def interleave_gate_up(w_gate: torch.Tensor, w_up: torch.Tensor) -> torch.Tensor
     return torch.cat([g, u], dim=2).reshape(K, 2 * C).contiguous()
 
 
+class PackedWeight:
+    """A [K, N] weight pre-packed (once, at load) into the GEMM's streaming
+    order: one 16 KB block per (128-column tile t, 64-row k-step s), blocks
+    ordered [t][s], each block in the tcgen05 canonical no-swizzle MN-major
+    layout [k-group 8][m-group 16][k 8][m 8].  The kernel moves a block with
+    ONE 1-D bulk copy straight into the UMMA operand layout, and a CTA's
+    stream-K range is one contiguous region of HBM."""
+
+    def __init__(self, w: torch.Tensor):
+        K, n = w.shape
+        if n % 128 or K % 64:
+            raise ValidationError("packed weights need N % 128 == 0 and K % 64 == 0")
+        self.K, self.N = K, n
+        blocks = w.reshape(K // 64, 8, 8, n // 128, 16, 8)       # s, kg, kr, t, mg, mc
+        self.panels = blocks.permute(3, 0, 1, 4, 2, 5).contiguous()  # t, s, kg, mg, kr, mc
+
+    def unpack(self) -> torch.Tensor:
+        return self.panels.permute(1, 2, 4, 0, 3, 5).reshape(self.K, self.N)
+
+
 class SkinnyGemm:
     """Workspace + semaphores for ``fs_gemm_skinny`` on one device (shared
     by all projections of an engine; launches are stream-ordered)."""
@@ -46,15 +66,18 @@ class SkinnyGemm:
             raise ValidationError("cannot size the GEMM workspace")
         self.max_n = max_n
         self.ws = torch.empty(floats, dtype=torch.float32, device=self.device)
-        self.sems = torch.zeros(max(1, max_n // 128), dtype=torch.int32, device=self.device)
+        self.sems = torch.zeros(2 * max(1, max_n // 128), dtype=torch.int32, device=self.device)
 
-    def __call__(self, x: torch.Tensor, w: torch.Tensor, out: torch.Tensor,
+    def __call__(self, x: torch.Tensor, w, out: torch.Tensor,
                  epilogue: int = STORE, res: torch.Tensor = None) -> torch.Tensor:
-        if x.dtype != torch.bfloat16 or w.dtype != torch.bfloat16 or out.dtype != torch.bfloat16:
+        """``w``: a [K, N] row-major bf16 matrix or a :class:`PackedWeight`."""
+        packed = isinstance(w, PackedWeight)
+        wt = w.panels if packed else w
+        if x.dtype != torch.bfloat16 or wt.dtype != torch.bfloat16 or out.dtype != torch.bfloat16:
             raise ValidationError("skinny GEMM operands must be bf16")
         rows, K = x.shape
-        Kw, n = w.shape
-        if Kw != K or x.stride(1) != 1 or w.stride(1) != 1 or out.stride(1) != 1:
+        Kw, n = (w.K, w.N) if packed else w.shape
+        if Kw != K or x.stride(1) != 1 or wt.stride(-1) != 1 or out.stride(1) != 1:
             raise ValidationError("skinny GEMM: shape / layout mismatch")
         if n > self.max_n:
             raise ValidationError(f"N={n} exceeds the workspace sized for {self.max_n}")
@@ -67,7 +90,8 @@ class SkinnyGemm:
             xs, os = x[r0:r0 + r], out[r0:r0 + r]
             rs = res[r0:r0 + r] if res is not None else None
             N.check(N.lib.fs_gemm_skinny(
-                N.ptr(xs), x.stride(0), r, K, N.ptr(w), w.stride(0), n, N.ptr(os), out.stride(0),
+                N.ptr(xs), x.stride(0), r, K, N.ptr(wt), 128 if packed else wt.stride(0),
+                1 if packed else 0, n, N.ptr(os), out.stride(0),
                 N.ptr(rs), res.stride(0) if res is not None else 0, epilogue, N.ptr(self.ws),
                 ws_floats, N.ptr(self.sems), self.index, stream), "fs_gemm_skinny")
         return out

@@ -115,7 +115,7 @@ class HybridDecodeRank:
 
     def __init__(self, model: ModelSpec, owner, rank: int, routing, batch: int, capacity: int,
                  device=None, seed: int = 0, group=None, page_order: str = "contiguous",
-                 config: int = 0, mlp: bool = False, shard_owner=None):
+                 config: int = 0, mlp: bool = False, shard_owner=None, gemm: str = "cublas"):
         if model.head_dim != N.HEAD_DIM:
             raise ValidationError(f"head_dim must be {N.HEAD_DIM} for the CUDA path")
         self.model = model
@@ -164,7 +164,32 @@ class HybridDecodeRank:
                 self.w_d[layer].copy_(d)
             self.h = torch.empty((batch, 2 * C), dtype=torch.bfloat16, device=dev)
             self.act = torch.empty((batch, C), dtype=torch.bfloat16, device=dev)
+        if gemm not in ("cublas", "tcgen05"):
+            raise ValidationError(f"unknown gemm backend {gemm!r}")
+        self.gemm = gemm
+        if gemm == "tcgen05":
+            self._use_skinny()
         self._graph = None
+
+    def _use_skinny(self) -> None:
+        """Projections through the hand-written tcgen05 GEMM: weights packed
+        once into its streaming layout; gate/up interleaved for the fused
+        SwiGLU epilogue."""
+        from .gemm import PackedWeight, SkinnyGemm, interleave_gate_up
+        L = self.model.num_layers
+        self.p_qkv = [PackedWeight(self.wqkv[l]) for l in range(L)]
+        self.p_o = [PackedWeight(self.wo[l]) for l in range(L)]
+        widest = max(self.wqkv.shape[2], self.wo.shape[2])
+        if self.mlp and len(self.ffn_cols):
+            C = len(self.ffn_cols)
+            self.p_gu = [PackedWeight(interleave_gate_up(self.w_gu[l, :, :C], self.w_gu[l, :, C:]))
+                         for l in range(L)]
+            self.p_d = [PackedWeight(self.w_d[l]) for l in range(L)]
+            widest = max(widest, 2 * C, self.w_d.shape[2])
+            del self.w_gu, self.w_d
+        del self.wqkv, self.wo
+        torch.cuda.empty_cache()
+        self.skinny = SkinnyGemm(widest, self.device)
 
     # ------------------------------------------------------------------ api --
     def set_lengths(self, lens) -> None:
@@ -181,6 +206,12 @@ class HybridDecodeRank:
         """This rank's pre-exchange attention contribution of ``layer`` for
         the current ``self.x``: ``o @ Wo_g`` [B, hidden] (into ``self.part``)."""
         B, S, hd = self.batch, self.n_slots, self.model.head_dim
+        if self.gemm == "tcgen05":
+            from .gemm import STORE
+            self.skinny(self.x, self.p_qkv[layer], self.qkv, STORE)
+            self.cache.decode_layer_fused(layer, self.qkv, self.o)
+            self.skinny(self.o.view(B, S * self.qpk * hd), self.p_o[layer], self.part, STORE)
+            return self.part
         torch.matmul(self.x, self.wqkv[layer], out=self.qkv)         # cuBLAS
         self.cache.decode_layer_fused(layer, self.qkv, self.o)       # K1 (+K2, +K3)
         torch.matmul(self.o.view(B, S * self.qpk * hd), self.wo[layer], out=self.part)
@@ -196,12 +227,44 @@ class HybridDecodeRank:
         """This rank's pre-exchange MLP contribution (its FFN shards)."""
         if not len(self.ffn_cols):
             return self.part.zero_()
+        if self.gemm == "tcgen05":
+            from .gemm import STORE, SWIGLU
+            self.skinny(self.x, self.p_gu[layer], self.act, SWIGLU)
+            self.skinny(self.act, self.p_d[layer], self.part, STORE)
+            return self.part
         torch.matmul(self.x, self.w_gu[layer], out=self.h)
         self._swiglu()
         torch.matmul(self.act, self.w_d[layer], out=self.part)
         return self.part
 
+    def _layers_skinny(self) -> None:
+        from .gemm import RESIDUAL, STORE, SWIGLU
+        B, S, hd = self.batch, self.n_slots, self.model.head_dim
+        x, o2, g = self.x, self.o.view(B, S * self.qpk * hd), self.skinny
+        for layer in range(self.model.num_layers):
+            g(x, self.p_qkv[layer], self.qkv, STORE)
+            self.cache.decode_layer_fused(layer, self.qkv, self.o)
+            if self.group is None:
+                g(o2, self.p_o[layer], x, RESIDUAL)
+            else:
+                g(o2, self.p_o[layer], self.part, STORE)
+                torch.distributed.all_reduce(self.part, group=self.group)
+                x.add_(self.part)
+            if self.mlp and len(self.ffn_cols):
+                g(x, self.p_gu[layer], self.act, SWIGLU)
+                if self.group is None:
+                    g(self.act, self.p_d[layer], x, RESIDUAL)
+                else:
+                    g(self.act, self.p_d[layer], self.part, STORE)
+            if self.mlp and self.group is not None:
+                if not len(self.ffn_cols):
+                    self.part.zero_()
+                torch.distributed.all_reduce(self.part, group=self.group)
+                x.add_(self.part)
+
     def _layers(self) -> None:
+        if self.gemm == "tcgen05":
+            return self._layers_skinny()
         B, S, hd = self.batch, self.n_slots, self.model.head_dim
         x, o2 = self.x, self.o.view(B, S * self.qpk * hd)
         for layer in range(self.model.num_layers):
@@ -224,10 +287,17 @@ class HybridDecodeRank:
 
     def launches_per_step(self) -> int:
         """Our kernel launches per step: the fused decode launch per layer,
-        plus the swiglu launch per layer with the MLP."""
-        return self.model.num_layers * (2 if self.mlp and len(self.ffn_cols) else 1)
+        plus the swiglu launch per layer with the MLP (cuBLAS GEMMs), or the
+        decode + 4 tcgen05 GEMM launches per layer (gemm="tcgen05")."""
+        has_mlp = self.mlp and len(self.ffn_cols)
+        if self.gemm == "tcgen05":
+            return self.model.num_layers * (5 if has_mlp else 3)
+        return self.model.num_layers * (2 if has_mlp else 1)
 
     def weight_bytes(self) -> int:
+        if self.gemm == "tcgen05":
+            ws = self.p_qkv + self.p_o + (getattr(self, "p_gu", []) + getattr(self, "p_d", []))
+            return 2 * sum(w.panels.numel() for w in ws)
         n = self.wqkv.numel() + self.wo.numel()
         if self.mlp:
             n += self.w_gu.numel() + self.w_d.numel()

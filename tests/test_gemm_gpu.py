@@ -74,3 +74,23 @@ def test_validation():
     out = torch.zeros((4, 128), device="cuda", dtype=torch.bfloat16)
     with pytest.raises(ValidationError):
         SkinnyGemm(128)(x, w, out)
+
+
+@pytest.mark.parametrize("K,N,epi", [(4096, 1280, 0), (1024, 4096, 1), (2048, 896, 2)])
+def test_packed_panels_match_row_major(K, N, epi):
+    from paper_2511_14116_b200.gemm import PackedWeight, SkinnyGemm, interleave_gate_up
+    g = torch.Generator(device="cuda").manual_seed(K + N)
+    x = torch.randn((64, K), device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn((K, N), device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+    if epi == 2:
+        w = interleave_gate_up(w[:, :N // 2], w[:, N // 2:])
+    pw = PackedWeight(w)
+    assert torch.equal(pw.unpack(), w)
+    n_out = N // 2 if epi == 2 else N
+    base = torch.randn((64, n_out), device="cuda", generator=g).to(torch.bfloat16)
+    a, b = base.clone(), base.clone()
+    gemm = SkinnyGemm(N)
+    gemm(x, w, a, epi)
+    gemm(x, pw, b, epi)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
