@@ -29,6 +29,11 @@
  *   fs_decode_attention <- the attention half of refexec.parallel_forward
  *                          (TP heads on owners, DP heads on routed rank)
  *                                                          refexec.py:281-297, 85-103
+ *   fs_prefill_attention <- the multi-row (chunked-prefill) form of
+ *                          refexec._head_attention for Alg. 1 batches
+ *                          (scheduler.build_prefill_batch) refexec.py:85-103,
+ *                                                          scheduler.py:189-245
+ *   fs_plan_prefill_tiles <- (new) host tile/split planner of that launch
  *   fs_kv_write / fs_kv_read <- (new) KV append into / read from pages
  *   fs_pages_gather     <- recovery.advance_backup executed as an incremental
  *                          page copy to pinned host       recovery.py:193-247
@@ -151,6 +156,58 @@ int64_t fs_decode_partial_slots(int device, int32_t n_items, int32_t config);
  * done in-kernel by the item's last warp.  ONE launch.  Output blocks not
  * named by any item are untouched. */
 int fs_decode_attention(const fs_decode_desc *d, void *stream);
+
+/* K8: paged chunked-prefill GQA attention.  Item i is one (kv head,
+ * request chunk): item_len[i] new tokens at prompt positions item_start[i]
+ * .. item_start[i]+item_len[i]-1 of block-table row item_seq[i] (their K/V
+ * already in the pages); chunk token j attends causally, including itself,
+ * to positions 0..item_start[i]+j (refexec.py:92-97).  A tile = up to
+ * fs_prefill_tokens_per_tile(q_per_kv) consecutive chunk tokens x all
+ * q_per_kv heads (64 query rows) over the KV page range [page0, page1);
+ * tile_slot < 0 -> the tile covers its whole causal range and writes the
+ * output; otherwise it writes a partial (O/l, log2-sum-exp) to that slot and
+ * the combine list merges slots comb_slot0 .. +comb_nsplit-1 of each
+ * (item, tok0) in the same call.  Tiles come from fs_plan_prefill_tiles. */
+typedef struct fs_prefill_desc {
+    const void *q;             /* bf16: block of (item i, token j) at element
+                                  item_qoff[i] + j*q_stride, q_per_kv x 128 */
+    void *out;                 /* bf16 (fp32 if out_fp32): item_ooff[i] +
+                                  j*o_stride                                */
+    int64_t q_stride, o_stride;
+    int32_t out_fp32;
+    const void *kv_pool;
+    const int32_t *block_table;
+    int64_t bt_stride;
+    const int32_t *item_seq, *item_start, *item_len, *item_qoff, *item_ooff;
+    const int32_t *tile_item, *tile_tok0, *tile_page0, *tile_page1, *tile_slot;
+    int32_t n_tiles;
+    const int32_t *comb_item, *comb_tok0, *comb_slot0, *comb_nsplit;
+    int32_t n_comb;
+    int32_t q_per_kv;          /* 1..8                                      */
+    float scale;
+    float *part_o;             /* [partial_slots][64][128] fp32             */
+    float *part_lse;           /* [partial_slots][64]                       */
+    int64_t partial_slots;
+} fs_prefill_desc;
+
+/* chunk tokens per 64-row prefill tile (64 / q_per_kv), or <0 */
+int fs_prefill_tokens_per_tile(int q_per_kv);
+
+/* Host planner of the K8 launch: token tiles of every item, each split into
+ * equal KV page ranges so the grid has >= ~target_units similar-sized
+ * tiles (pass 4*SMs); heaviest tiles first.  Output arrays sized by the
+ * caller with max_tiles / max_comb entries; returns the tile count in
+ * *n_tiles, combine groups in *n_comb and the partial slots used in
+ * *n_slots.  FS_EVALIDATION if the arrays are too small. */
+int fs_plan_prefill_tiles(int32_t n_items, const int32_t *item_start, const int32_t *item_len,
+                          int32_t q_per_kv, int32_t target_units, int32_t max_tiles,
+                          int32_t *tile_item, int32_t *tile_tok0, int32_t *tile_page0,
+                          int32_t *tile_page1, int32_t *tile_slot, int32_t *n_tiles,
+                          int32_t max_comb, int32_t *comb_item, int32_t *comb_tok0,
+                          int32_t *comb_slot0, int32_t *comb_nsplit, int32_t *n_comb,
+                          int32_t *n_slots);
+
+int fs_prefill_attention(const fs_prefill_desc *d, void *stream);
 
 /* K3: write n_tok (K,V) rows into pages: token t goes to sequence
  * tok_seq[t] at position tok_pos[t]; its K/V are rows tok_src[t] of

@@ -37,6 +37,19 @@ def head_decode(q, k, v, scale):
     return w @ v
 
 
+def head_prefill(q, k, v, start, scale):
+    """Chunked-prefill rows of ``_head_attention`` (refexec.py:85-103):
+    q: [n, qpk, hd] for prompt positions start..start+n-1; k, v: [>= start+n,
+    hd].  Row t attends to positions 0..start+t (causal, including self).
+    Returns [n, qpk, hd] float64."""
+    q = np.asarray(q, dtype=np.float64)
+    n = q.shape[0]
+    out = np.empty(q.shape, dtype=np.float64)
+    for t in range(n):
+        out[t] = head_decode(q[t], k[:start + t + 1], v[:start + t + 1], scale)
+    return out
+
+
 def paged_decode(q_rows, k_pool, v_pool, block_table, item_seq, item_len,
                  item_qrow, n_out_rows, scale, page_size=16):
     """Paged GQA decode over work items.

@@ -29,7 +29,8 @@ from failsafe.recovery import (BackupState, advance_backup,  # noqa: E402
 from failsafe.refexec import (ToyLayerWeights, ToyModelWeights,  # noqa: E402
                               _head_attention, _segments, parallel_forward,
                               reference_forward)
-from failsafe.scheduler import SchedulerState, route_request  # noqa: E402
+from failsafe.scheduler import (SchedulerState, build_prefill_batch,  # noqa: E402
+                                fifo_chunked_prefill, round_robin_route, route_request)
 
 OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                    "tests", "golden")
@@ -154,6 +155,89 @@ def gen_routing():
     interleaved = {"requests": [[r.input_len, r.output_len] for r in reqs], "events": events,
                    "workload": [st.workload[r] for r in range(3)]}
     return {"cases": cases, "interleaved": interleaved}
+
+
+def gen_batches():
+    """Adaptive (Alg. 1) and FIFO chunked-prefill batches: random backlogs
+    routed by the load-aware or round-robin router, then batches drained
+    until the queues are empty, with arrivals and decode accounting
+    interleaved (scheduler.py:139-281)."""
+    rng = random.Random(2024)
+    cases = []
+    for ci in range(80):
+        n = rng.randint(1, 8)
+        budget = rng.choice([1, 2, 3, 7, 16, 64, 256, 2048])
+        max_in = 900 if budget >= 64 else 40
+        kappa = rng.choice([1.0 / 512.0, 1.0 / 512.0, 1.0, 0.25])
+        sched = "fifo" if ci % 4 == 3 else "load_aware"
+        st = SchedulerState(token_budget=budget, rank_set=tuple(range(n)), kappa=kappa,
+                            include_decode_in_workload=rng.random() < 0.8)
+        reqs, events = [], []
+        waves = rng.randint(1, 3)
+        for wave in range(waves):
+            for _ in range(rng.randint(0 if wave else 1, 10)):
+                i = len(reqs)
+                r = Request(id=i, arrival_time=0.0, input_len=rng.randint(1, max_in),
+                            output_len=rng.randint(1, 50))
+                reqs.append(r)
+                rank = (route_request if sched == "load_aware" else round_robin_route)(st, r)
+                events.append({"route": [i, r.input_len, r.output_len], "rank": rank})
+            for _ in range(rng.randint(1, 4)):
+                b = (build_prefill_batch if sched == "load_aware" else fifo_chunked_prefill)(st)
+                for rid, start, length in b.entries:
+                    reqs[rid].tokens_prefilled += length
+                events.append({"batch": [list(e) for e in b.entries],
+                               "per_rank_load": [b.per_rank_load[g] for g in range(n)],
+                               "workload": [st.workload[g] for g in range(n)]})
+                # one decode token for finished prefills
+                for r in reqs:
+                    if r.tokens_prefilled == r.input_len and r.tokens_decoded < r.output_len:
+                        r.tokens_decoded += 1
+                        st.note_decode_token(r, r.dp_rank)
+                        events.append({"decode": [r.id, r.dp_rank]})
+        for _ in range(12):  # drain (bounded: keeps the fixture small)
+            if not st.has_prefill_work():
+                break
+            b = (build_prefill_batch if sched == "load_aware" else fifo_chunked_prefill)(st)
+            if not b.entries:
+                break
+            events.append({"batch": [list(e) for e in b.entries],
+                           "per_rank_load": [b.per_rank_load[g] for g in range(n)],
+                           "workload": [st.workload[g] for g in range(n)]})
+        cases.append({"n": n, "budget": budget, "kappa": kappa, "scheduler": sched,
+                      "include_decode": st.include_decode_in_workload, "events": events})
+    return {"cases": cases}
+
+
+def gen_prefill():
+    """Chunked-prefill rows of ``_head_attention`` (refexec.py:85-103): the
+    rows [start, start+n) of each request attend causally (including self)
+    to the request's prefix; GQA by tied identity K/V weights, bf16-exact
+    inputs (as gen_decode)."""
+    rng = np.random.default_rng(777)
+    hd = 128
+    cases = []
+    for qpk, seq_lens, chunks in ((1, [40, 17], [(8, 32), (0, 17)]),
+                                  (4, [64, 33, 5], [(16, 20), (1, 31), (0, 5)]),
+                                  (8, [90, 24], [(60, 30), (0, 24)]),
+                                  (2, [160], [(100, 60)])):
+        x = bf16_round(rng.standard_normal((sum(seq_lens), hd)))
+        eye = np.eye(hd)
+        diags = [np.diag(rng.choice([-2.0, -1.0, -0.5, 0.5, 1.0, 2.0], size=hd))
+                 for _ in range(qpk)]
+        lw = ToyLayerWeights(wq=np.stack(diags), wk=np.stack([eye] * qpk),
+                             wv=np.stack([eye] * qpk), wo=np.stack([eye] * qpk),
+                             w_up=np.zeros((2, hd)), w_down=np.zeros((hd, 2)))
+        segs = _segments(x.shape[0], seq_lens)
+        rows = np.zeros(x.shape[0], dtype=bool)
+        for (s, e), (c0, cn) in zip(segs, chunks):
+            rows[s + c0:s + c0 + cn] = True
+        outs = [_head_attention(lw, h, x, segs, rows=rows) for h in range(qpk)]
+        sel = np.flatnonzero(rows)
+        cases.append({"qpk": qpk, "seq_lens": seq_lens, "chunks": chunks, "x": x.tolist(),
+                      "diag": [np.diag(d).tolist() for d in diags],
+                      "out": [[outs[h][t].tolist() for h in range(qpk)] for t in sel]})
+    return {"head_dim": hd, "cases": cases}
 
 
 def toy_model(L, H, shards, qpk=1):
@@ -325,9 +409,13 @@ def gen_decode():
 
 def main():
     os.makedirs(OUT, exist_ok=True)
-    for name, fn in (("placement", gen_placement), ("routing", gen_routing),
-                     ("recovery", gen_recovery), ("forward", gen_forward),
-                     ("decode", gen_decode)):
+    gens = (("placement", gen_placement), ("routing", gen_routing),
+            ("recovery", gen_recovery), ("forward", gen_forward), ("decode", gen_decode),
+            ("batches", gen_batches), ("prefill", gen_prefill))
+    only = sys.argv[1:]
+    for name, fn in gens:
+        if only and name not in only:
+            continue
         data = fn()
         data["_generated_by"] = ("oracle/gen_golden.py from the live reference "
                                  f"failsafe {getattr(failsafe, '__version__', '?')}")

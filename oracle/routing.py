@@ -60,3 +60,38 @@ def route_sequence(requests, ranks, kappa=KAPPA, include_decode=True):
     r = Router(ranks, kappa, include_decode)
     out = [r.route(i, o) for i, o in requests]
     return out, dict(r.load)
+
+
+def prefill_schedule(queues, budget, kappa=KAPPA, workload=None):
+    """Alg. 1 adaptive chunked prefill, restated literally
+    (scheduler.py:189-245): ``queues`` maps rank -> list of
+    ``[request, next token, end]`` spans (mutated); each step feeds ONE token
+    to ``argmin (load, rank)`` over ranks with queued tokens; a token at
+    prompt index i costs ``1 + kappa*i`` (scheduler.py:24-35).  Returns
+    (entries, per-rank load) with entries in first-scheduled order;
+    ``workload`` (rank -> pending cost) is decremented per token, clamped
+    at zero, as the reference does."""
+    ranks = sorted(queues)
+    loads = {r: 0.0 for r in ranks}
+    chunks = {}
+    taken = 0
+    while taken < budget:
+        live = [r for r in ranks if queues[r]]
+        if not live:
+            break
+        r = min(live, key=lambda g: (loads[g], g))
+        span = queues[r][0]
+        rid, idx = span[0], span[1]
+        span[1] += 1
+        if span[1] >= span[2]:
+            queues[r].pop(0)
+        cost = 1.0 + kappa * idx
+        loads[r] = loads[r] + cost
+        if workload is not None:
+            workload[r] = max(0.0, workload[r] - cost)
+        if rid in chunks:
+            chunks[rid][1] += 1
+        else:
+            chunks[rid] = [idx, 1]
+        taken += 1
+    return [(rid, s, n) for rid, (s, n) in chunks.items()], loads

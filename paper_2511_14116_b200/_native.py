@@ -42,6 +42,23 @@ class DecodeDesc(C.Structure):
     ]
 
 
+class PrefillDesc(C.Structure):
+    """Mirror of ``fs_prefill_desc``."""
+
+    _fields_ = [
+        ("q", C.c_void_p), ("out", C.c_void_p), ("q_stride", C.c_int64), ("o_stride", C.c_int64),
+        ("out_fp32", C.c_int32), ("kv_pool", C.c_void_p), ("block_table", C.c_void_p), ("bt_stride", C.c_int64),
+        ("item_seq", C.c_void_p), ("item_start", C.c_void_p), ("item_len", C.c_void_p),
+        ("item_qoff", C.c_void_p), ("item_ooff", C.c_void_p),
+        ("tile_item", C.c_void_p), ("tile_tok0", C.c_void_p), ("tile_page0", C.c_void_p),
+        ("tile_page1", C.c_void_p), ("tile_slot", C.c_void_p), ("n_tiles", C.c_int32),
+        ("comb_item", C.c_void_p), ("comb_tok0", C.c_void_p), ("comb_slot0", C.c_void_p),
+        ("comb_nsplit", C.c_void_p), ("n_comb", C.c_int32), ("q_per_kv", C.c_int32),
+        ("scale", C.c_float), ("part_o", C.c_void_p), ("part_lse", C.c_void_p),
+        ("partial_slots", C.c_int64),
+    ]
+
+
 # name -> (restype, argtypes)
 _SIGS = {
     "fs_abi_version": (C.c_int, []),
@@ -56,6 +73,11 @@ _SIGS = {
     "fs_plan_pages": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
     "fs_decode_partial_slots": (C.c_int64, [C.c_int, C.c_int32, C.c_int32]),
     "fs_decode_attention": (C.c_int, [C.POINTER(DecodeDesc), C.c_void_p]),
+    "fs_prefill_tokens_per_tile": (C.c_int, [C.c_int]),
+    "fs_plan_prefill_tiles": (C.c_int, [C.c_int32, _i32p, _i32p, C.c_int32, C.c_int32, C.c_int32,
+                                        _i32p, _i32p, _i32p, _i32p, _i32p, _i32p, C.c_int32,
+                                        _i32p, _i32p, _i32p, _i32p, _i32p, _i32p]),
+    "fs_prefill_attention": (C.c_int, [C.POINTER(PrefillDesc), C.c_void_p]),
     "fs_kv_write": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                               C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64,
                               C.c_void_p]),

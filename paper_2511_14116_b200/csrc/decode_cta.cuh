@@ -180,8 +180,13 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_cta_kernel(const DecodeP
                 o[mt][2] *= al0;
                 o[mt][3] *= al1;
             }
-            const uint32_t pb0 = movmatrix_t(pack_bf16(p0, p1));
-            const uint32_t pb1 = movmatrix_t(pack_bf16(p2, p3));
+            // P^T as bf16 hi + lo parts: bf16 P alone costs ~1.5e-3 mean relative
+            // error on long contexts (north star: 1e-3); the tensor pipe has the slack
+            uint32_t h01, l01, h23, l23;
+            split_bf16x2(p0, p1, h01, l01);
+            split_bf16x2(p2, p3, h23, l23);
+            const uint32_t pb0 = movmatrix_t(h01), pb1 = movmatrix_t(h23);
+            const uint32_t pl0 = movmatrix_t(l01), pl1 = movmatrix_t(l23);
             {
                 const int i = lane >> 3;
                 const uint32_t r = (lane & 7) + ((i >> 1) << 3);
@@ -190,6 +195,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_cta_kernel(const DecodeP
                     uint32_t a0, a1, a2, a3;
                     ldsm_x4_t(vb + swz(r, 2 * mt + (i & 1)), a0, a1, a2, a3);
                     mma_bf16(o[mt], a0, a1, a2, a3, pb0, pb1);
+                    mma_bf16(o[mt], a0, a1, a2, a3, pl0, pl1);
                 }
             }
             __syncwarp();

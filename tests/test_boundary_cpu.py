@@ -84,3 +84,52 @@ def test_errors_map_to_reference_classes():
         make_placement("bogus", m, range(2))
     with pytest.raises(ValidationError):
         make_placement("hybrid", m, [])
+
+
+def test_prefill_tile_planner():
+    """fs_plan_prefill_tiles (host code, no GPU): every chunk token lies in
+    exactly one token tile, each tile's page splits tile its causal range
+    [0, ceil((start + last + 1) / 16)) exactly once, slots are unique, and
+    tiles come heaviest first."""
+    import ctypes as C
+    from paper_2511_14116_b200 import _native as N
+    rng = np.random.default_rng(0)
+    for qpk in (1, 3, 4, 8):
+        tpt = N.lib.fs_prefill_tokens_per_tile(qpk)
+        assert tpt == 64 // qpk
+        starts = rng.integers(0, 5000, size=12).astype(np.int32)
+        lens = rng.integers(0, 300, size=12).astype(np.int32)
+        for target in (1, 600, 100000):
+            cap = 20000
+            arr = {k: (C.c_int32 * cap)() for k in ("i", "t", "a", "b", "s", "ci", "ct", "c0", "cn")}
+            nt, nc, ns = C.c_int32(), C.c_int32(), C.c_int32()
+            P = C.POINTER(C.c_int32)
+            rc = N.lib.fs_plan_prefill_tiles(
+                12, starts.ctypes.data_as(P), lens.ctypes.data_as(P), qpk, target, cap,
+                arr["i"], arr["t"], arr["a"], arr["b"], arr["s"], C.byref(nt), cap, arr["ci"],
+                arr["ct"], arr["c0"], arr["cn"], C.byref(nc), C.byref(ns))
+            assert rc == 0
+            tiles = [tuple(arr[k][j] for k in "itabs") for j in range(nt.value)]
+            widths = [b - a for _, _, a, b, _ in tiles]
+            assert widths == sorted(widths, reverse=True)
+            cover = {}
+            for i, t0, a, b, s in tiles:
+                cover.setdefault((i, t0), []).append((a, b, s))
+            want = {(i, t0) for i in range(12) for t0 in range(0, lens[i], tpt)}
+            assert set(cover) == want
+            slots = [s for *_, s in tiles if s >= 0]
+            assert len(slots) == len(set(slots)) == ns.value
+            for (i, t0), parts in cover.items():
+                last = min(t0 + tpt, lens[i]) - 1
+                pages = (starts[i] + last + 1 + 15) // 16
+                parts.sort()
+                assert parts[0][0] == 0 and parts[-1][1] == pages
+                assert all(p[1] == q[0] for p, q in zip(parts, parts[1:]))
+                assert (len(parts) == 1) == (parts[0][2] < 0)
+            assert nc.value == sum(1 for p in cover.values() if len(p) > 1)
+        # too small an output array is a ValidationError-class status
+        one = (C.c_int32 * 1)()
+        rc = N.lib.fs_plan_prefill_tiles(12, starts.ctypes.data_as(P), lens.ctypes.data_as(P),
+                                         qpk, 1, 1, one, one, one, one, one, C.byref(nt), 1,
+                                         one, one, one, one, C.byref(nc), C.byref(ns))
+        assert rc == N.FS_EVALIDATION

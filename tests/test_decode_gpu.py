@@ -402,3 +402,31 @@ def test_engine_graph_capture_replays_identically():
     e.capture()
     graphed = e.step(x0.cuda()).clone()
     assert torch.equal(eager, graphed)
+
+
+@pytest.mark.parametrize("qpk", [4, 8])
+def test_decode_long_context_per_item_tolerance(qpk):
+    """The tolerance holds per long item, not only diluted over a launch:
+    bf16 P alone gives ~1.5e-3 mean-rel at 4k context; the kernels carry P
+    as a bf16 hi/lo pair."""
+    from oracle.attention import head_decode
+    from oracle.placement import owner_table
+    owner = owner_table("hybrid", 1, 8, range(8))
+    lens = [4096, 3000, 8192]
+    routing = {r: 0 for r in range(3)}
+    for config in (0, 7):
+        work, cache = _build(owner, 0, routing, lens, qpk, config=config)
+        gen = torch.Generator().manual_seed(qpk + config)
+        kv = _fill(cache, work, lens, gen)
+        n_rows = 3 * work.n_slots
+        q = _bf16(torch.randn((n_rows, qpk, 128), generator=gen))
+        out = torch.zeros((n_rows, qpk, 128), dtype=torch.float32, device="cuda")
+        cache.decode_layer(0, q.cuda(), out)
+        torch.cuda.synchronize()
+        got = out.cpu().numpy()
+        qn = q.double().numpy()
+        for i in range(work.n_items):
+            r, j = work.item_req[i], work.item_slot[i]
+            row = r * work.n_slots + j
+            k, v = kv[i]
+            _close(got[row], head_decode(qn[row], k[:lens[r]], v[:lens[r]], 1 / math.sqrt(128)))

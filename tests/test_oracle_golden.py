@@ -188,3 +188,19 @@ def test_oracle_against_live_reference_random():
             tab = [[(-1 if a.owner_of(h) is None else a.owner_of(h)) for h in range(H)]
                    for a in plan.per_layer]
             assert OP.owner_table(mode, L, H, alive) == tab
+
+
+def test_prefill_restatement(golden):
+    """Chunked-prefill rows of the live _head_attention (gen_prefill)."""
+    g = golden("prefill")
+    hd = g["head_dim"]
+    for c in g["cases"]:
+        x = np.array(c["x"])
+        start, k = 0, 0
+        for length, (c0, cn) in zip(c["seq_lens"], c["chunks"]):
+            seg = x[start:start + length]
+            q = np.stack([seg[c0:c0 + cn] * np.array(d) for d in c["diag"]], axis=1)
+            out = OA.head_prefill(q, seg, seg, c0, 1.0 / np.sqrt(hd))
+            np.testing.assert_allclose(out, np.array(c["out"][k:k + cn]), rtol=0, atol=1e-12)
+            start += length
+            k += cn
