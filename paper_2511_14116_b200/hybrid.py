@@ -115,7 +115,8 @@ class HybridDecodeRank:
 
     def __init__(self, model: ModelSpec, owner, rank: int, routing, batch: int, capacity: int,
                  device=None, seed: int = 0, group=None, page_order: str = "contiguous",
-                 config: int = 0, mlp: bool = False, shard_owner=None, gemm: str = "cublas"):
+                 config: int = 0, mlp: bool = False, shard_owner=None, gemm: str = "cublas",
+                 request_capacity=None):
         if model.head_dim != N.HEAD_DIM:
             raise ValidationError(f"head_dim must be {N.HEAD_DIM} for the CUDA path")
         self.model = model
@@ -127,7 +128,8 @@ class HybridDecodeRank:
         self.qpk = model.q_heads_per_kv_head
         self.work = RankWork.build(np.asarray(owner, dtype=np.int32), rank, routing, batch)
         self.cache = PagedKVCache(self.work, capacity, self.qpk, self.device,
-                                  page_order=page_order, seed=seed, config=config)
+                                  page_order=page_order, seed=seed, config=config,
+                                  request_capacity=request_capacity)
         hd, hid, S = model.head_dim, model.hidden_dim, self.work.n_slots
         self.n_slots = S
         L = model.num_layers

@@ -101,7 +101,8 @@ class PagedKVCache:
     """
 
     def __init__(self, work: RankWork, capacity: int, q_per_kv: int, device=None,
-                 page_order: str = "contiguous", seed: int = 0, config: int = 0):
+                 page_order: str = "contiguous", seed: int = 0, config: int = 0,
+                 request_capacity=None):
         if not (1 <= q_per_kv <= N.MAX_Q_PER_KV):
             raise ValidationError(f"q_per_kv must be in [1, {N.MAX_Q_PER_KV}]")
         if capacity < 1:
@@ -115,13 +116,27 @@ class PagedKVCache:
             else torch.cuda.current_device()
         n_seq = work.n_items
         self.pages_per_seq = math.ceil(capacity / N.PAGE_TOKENS)
-        self.n_pages = max(1, n_seq * self.pages_per_seq)
+        if request_capacity is None:
+            seq_pages = np.full(n_seq, self.pages_per_seq, dtype=np.int64)
+        else:
+            # per-request token capacity (<= capacity): only those pages are
+            # backed; the rest of each block-table row is never addressed
+            cap = np.asarray(request_capacity, dtype=np.int64)
+            if cap.size and (cap.max() > capacity or cap.min() < 0):
+                raise ValidationError("request capacities must lie in [0, capacity]")
+            seq_pages = (cap[work.item_req] + N.PAGE_TOKENS - 1) // N.PAGE_TOKENS \
+                if n_seq else np.zeros(0, np.int64)
+        self.seq_tokens = seq_pages * N.PAGE_TOKENS
+        self.n_pages = max(1, int(seq_pages.sum()))
         ids = np.arange(self.n_pages, dtype=np.int64)
         if page_order == "shuffled":
             ids = np.random.default_rng(seed).permutation(self.n_pages)
         elif page_order != "contiguous":
             raise ValidationError(f"unknown page_order {page_order!r}")
-        bt = ids[:n_seq * self.pages_per_seq].reshape(max(n_seq, 0), self.pages_per_seq)
+        bt = np.zeros((max(n_seq, 0), self.pages_per_seq), dtype=np.int64)
+        cols = np.arange(self.pages_per_seq)
+        mask = cols[None, :] < seq_pages[:, None]
+        bt[mask] = ids[:int(seq_pages.sum())]
         dev = self.device
         self.pool = torch.empty((self.n_pages, N.PAGE_BYTES), dtype=torch.uint8, device=dev)
         self.block_table = torch.from_numpy(bt.astype(np.int32)).to(dev)

@@ -1,0 +1,324 @@
+"""The mixed prefill/decode serving iteration of one rank (BASELINE config 5).
+
+One iteration of the reference's serving loop (``Simulation._start_iteration``,
+simulation.py:404-443) combines an Alg. 1 prefill batch
+(``scheduler.build_prefill_batch``, scheduler.py:189-245: ``(request, chunk
+start, chunk length)`` entries under the token budget) with one decode token
+per resident request whose prefill finished.  This module executes that
+iteration for real on a rank of the hybrid-attention layout -- the same
+per-rank decomposition as ``parallel_forward`` (refexec.py:249-308): TP heads
+for every token, replicated (DP) heads only for tokens of requests routed to
+the rank, FFN shards the rank owns, partials summed over the ranks.
+
+Per layer, for the T tokens of the iteration (prefill chunk tokens first,
+then the decode tokens):
+
+1. ``[q|k|v] = x @ Wqkv_g`` for the rank's local KV-head slots (cuBLAS);
+2. K3 writes every served token's K/V into its pages (one launch);
+3. K8 ``fs_prefill_attention`` over the prefill items (one launch) and K1
+   ``fs_decode_attention`` over the decode items (one launch);
+4. ``o @ Wo_g`` (+ NCCL all-reduce over the alive ranks), residual;
+5. the TP MLP partial over the rank's FFN shards (+ all-reduce), residual.
+
+The host builds a :class:`StepPlan` per iteration (work tables of every
+layer, uploaded in one copy; K8 tile plans from the native planner); the
+device work is then launch-only.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .core import ValidationError
+from .hybrid import HybridDecodeRank
+from .prefill import PrefillLaunch
+
+
+@dataclass
+class StepBatch:
+    """One serving iteration: Alg. 1 prefill entries ``(request, start,
+    length)`` and decode tokens ``(request, position)`` -- the new token at
+    ``position`` attends positions ``0..position`` (refexec.py:97)."""
+
+    prefill: list = field(default_factory=list)
+    decode: list = field(default_factory=list)
+
+    @property
+    def num_tokens(self) -> int:
+        return sum(n for _, _, n in self.prefill) + len(self.decode)
+
+
+class StepPlan:
+    """Device work tables of one iteration on one rank (all layers)."""
+
+    def __init__(self, eng: "HybridServingRank", batch: StepBatch):
+        self.batch = batch
+        T = batch.num_tokens
+        if T > eng.max_tokens:
+            raise ValidationError(f"iteration has {T} tokens > max_tokens {eng.max_tokens}")
+        for r, s, n in batch.prefill:
+            if n < 1 or s < 0 or s + n > eng.request_capacity[r]:
+                raise ValidationError(f"prefill chunk {(r, s, n)} outside request capacity")
+        for r, pos in batch.decode:
+            if pos < 0 or pos + 1 > eng.request_capacity[r]:
+                raise ValidationError(f"decode token {(r, pos)} outside request capacity")
+        self.T = T
+        L, S, qpk, hd = eng.model.num_layers, eng.n_slots, eng.qpk, eng.model.head_dim
+        rw, ow = eng.row_width, S * qpk * hd
+        pre_row = np.cumsum([0] + [n for _, _, n in batch.prefill])[:-1]
+        Tp = int(sum(n for _, _, n in batch.prefill))
+        tok_seq, tok_pos, tok_src, kv_seg = [], [], [], [0]
+        dec = {k: [] for k in ("seq", "len", "qoff", "ooff")}
+        dec_seg = [0]
+        self.prefill = []
+        for layer in range(L):
+            idx = eng.item_index[layer]
+            pf = {k: [] for k in ("seq", "start", "len", "qoff", "ooff")}
+            for j in range(len(eng.work.slot_heads[layer])):
+                for e, (r, st, n) in enumerate(batch.prefill):
+                    it = int(idx[j, r])
+                    if it < 0:
+                        continue  # replicated head, request routed elsewhere
+                    row = int(pre_row[e])
+                    pf["seq"].append(it)
+                    pf["start"].append(st)
+                    pf["len"].append(n)
+                    pf["qoff"].append(row * rw + j * qpk * hd)
+                    pf["ooff"].append(row * ow + j * qpk * hd)
+                    tok_seq.append(np.full(n, it))
+                    tok_pos.append(np.arange(st, st + n))
+                    tok_src.append((row + np.arange(n)) * (rw // hd) + j)
+                for d, (r, pos) in enumerate(batch.decode):
+                    it = int(idx[j, r])
+                    if it < 0:
+                        continue
+                    row = Tp + d
+                    dec["seq"].append(it)
+                    dec["len"].append(pos + 1)
+                    dec["qoff"].append(row * rw + j * qpk * hd)
+                    dec["ooff"].append(row * ow + j * qpk * hd)
+                    tok_seq.append(np.array([it]))
+                    tok_pos.append(np.array([pos]))
+                    tok_src.append(np.array([row * (rw // hd) + j]))
+            kv_seg.append(sum(a.size for a in tok_seq))
+            dec_seg.append(len(dec["seq"]))
+            self.prefill.append(PrefillLaunch(eng.cache, pf["seq"], pf["start"], pf["len"],
+                                              pf["qoff"], pf["ooff"]) if pf["seq"] else None)
+        cat = (lambda xs: np.concatenate(xs).astype(np.int32) if xs else np.zeros(0, np.int32))
+        n_kv = kv_seg[-1]
+        n_dec = dec_seg[-1]
+        self.kv_seg = kv_seg
+        self.dec_seg = np.array(dec_seg, dtype=np.int32)
+        flat = np.concatenate([cat(tok_seq), cat(tok_pos), cat(tok_src),
+                               np.array(dec["seq"], np.int32), np.array(dec["len"], np.int32),
+                               np.array(dec["qoff"], np.int32), np.array(dec["ooff"], np.int32),
+                               self.dec_seg])
+        dev = eng.device
+        self._tab = torch.from_numpy(flat).to(dev)
+        o = 0
+        self._off = {}
+        for name, size in (("tok_seq", n_kv), ("tok_pos", n_kv), ("tok_src", n_kv),
+                           ("d_seq", n_dec), ("d_len", n_dec), ("d_qoff", n_dec),
+                           ("d_ooff", n_dec), ("d_seg", L + 1)):
+            self._off[name] = o
+            o += size
+        self.n_dec = n_dec
+        self.dec_sem = torch.zeros(max(1, n_dec), dtype=torch.int32, device=dev)
+        self.page_off = torch.zeros(n_dec + L, dtype=torch.int32, device=dev)
+        if n_dec:
+            N.check(N.lib.fs_plan_pages(self.ptr("d_len"), self.ptr("d_seg"), L,
+                                        N.ptr(self.page_off), _stream()), "fs_plan_pages")
+        self._descs = [self._decode_desc(eng, layer) for layer in range(L)]
+        # algorithmic KV bytes of the iteration on this rank (512 B per
+        # (head, token) read: decode items read len, prefill tiles their
+        # causal page range)
+        self.kv_read_bytes = 512 * int(np.sum(dec["len"])) + sum(
+            (p.kv_page_reads * N.PAGE_BYTES) for p in self.prefill if p is not None)
+        self.attn_flops = sum(p.flops for p in self.prefill if p is not None)
+
+    def ptr(self, name, index=0):
+        return N.C.c_void_p(self._tab.data_ptr() + 4 * (self._off[name] + index))
+
+    def _decode_desc(self, eng, layer):
+        a, b = int(self.dec_seg[layer]), int(self.dec_seg[layer + 1])
+        if a == b:
+            return None
+        d = N.DecodeDesc()
+        c = eng.cache
+        d.q = eng.qkv_s.data_ptr()
+        d.kv_pool = c.pool.data_ptr()
+        d.block_table = c.block_table.data_ptr()
+        d.bt_stride = c.pages_per_seq
+        d.item_seq = self.ptr("d_seq", a).value
+        d.item_len = self.ptr("d_len", a).value
+        d.item_qoff = self.ptr("d_qoff", a).value
+        d.item_ooff = self.ptr("d_ooff", a).value
+        d.page_off = self.page_off.data_ptr() + 4 * (a + layer)
+        d.kv_new = None
+        d.item_sem = self.dec_sem.data_ptr() + 4 * a
+        d.n_items = b - a
+        d.q_per_kv = eng.qpk
+        d.scale = 1.0 / math.sqrt(eng.model.head_dim)
+        d.out_fp32 = 0
+        d.out = eng.o_s.data_ptr()
+        d.part_o = eng.part_o.data_ptr()
+        d.part_lse = eng.part_lse.data_ptr()
+        d.partial_slots = eng.part_o.shape[0]
+        d.device = c.dev_index
+        d.config = c.config
+        return d
+
+
+def _stream():
+    return N.C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class HybridServingRank(HybridDecodeRank):
+    """One rank of the mixed prefill/decode iteration.
+
+    ``routing``: request -> GPU for every request of the serving window
+    (drives which requests' replicated heads live here); ``request_capacity``:
+    per-request KV token capacity (final context, ``Request.final_context_
+    tokens``, core.py:155-156) -- only those pages are backed; ``max_tokens``:
+    largest iteration (the token budget plus the decode batch).
+    """
+
+    def __init__(self, model, owner, rank: int, routing, request_capacity, max_tokens: int,
+                 device=None, seed: int = 0, group=None, mlp: bool = True, shard_owner=None,
+                 config: int = 0, page_order: str = "contiguous"):
+        cap = np.asarray(request_capacity, dtype=np.int64)
+        if cap.ndim != 1 or cap.size == 0 or cap.min() < 1:
+            raise ValidationError("request_capacity must list >= 1 token per request")
+        super().__init__(model, owner, rank, routing, int(cap.size), int(cap.max()),
+                         device=device, seed=seed, group=group, page_order=page_order,
+                         config=config, mlp=mlp, shard_owner=shard_owner,
+                         request_capacity=cap)
+        self.request_capacity = cap
+        self.max_tokens = int(max_tokens)
+        S, hd, qpk, hid = self.n_slots, model.head_dim, self.qpk, model.hidden_dim
+        self.row_width = S * (qpk + 2) * hd
+        dev = self.device
+        T = self.max_tokens
+        self.x_s = torch.zeros((T, hid), dtype=torch.bfloat16, device=dev)
+        self.qkv_s = torch.empty((T, self.row_width), dtype=torch.bfloat16, device=dev)
+        self.o_s = torch.zeros((T, S * qpk * hd), dtype=torch.bfloat16, device=dev)
+        self.part_s = torch.empty((T, hid), dtype=torch.bfloat16, device=dev)
+        if self.mlp and len(self.ffn_cols):
+            C = len(self.ffn_cols)
+            self.h_s = torch.empty((T, 2 * C), dtype=torch.bfloat16, device=dev)
+            self.act_s = torch.empty((T, C), dtype=torch.bfloat16, device=dev)
+        # decode partials: enough slots for every decode item of one layer
+        w = self.work
+        per_layer = max(int(w.seg_items[l + 1] - w.seg_items[l]) for l in range(model.num_layers))
+        slots = N.lib.fs_decode_partial_slots(self.cache.dev_index, per_layer, -1)
+        self.part_o = torch.empty((slots, qpk, hd), dtype=torch.float32, device=dev)
+        self.part_lse = torch.empty((slots, qpk), dtype=torch.float32, device=dev)
+        # (layer, slot, request) -> work item (= block-table row), -1 if the
+        # replicated head's request is routed elsewhere
+        self.item_index = []
+        for layer in range(model.num_layers):
+            idx = np.full((S, int(cap.size)), -1, dtype=np.int64)
+            a, b = int(w.seg_items[layer]), int(w.seg_items[layer + 1])
+            idx[w.item_slot[a:b], w.item_req[a:b]] = np.arange(a, b)
+            self.item_index.append(idx)
+
+    def plan(self, batch: StepBatch) -> StepPlan:
+        return StepPlan(self, batch)
+
+    # ------------------------------------------------------------ pieces --
+    def _attention(self, layer: int, plan: StepPlan) -> None:
+        T = plan.T
+        x, qkv, o = self.x_s[:T], self.qkv_s[:T], self.o_s[:T]
+        torch.matmul(x, self.wqkv[layer], out=qkv)                       # cuBLAS
+        a, b = plan.kv_seg[layer], plan.kv_seg[layer + 1]
+        if b > a:                                                        # K3
+            hd = self.model.head_dim
+            qw = self.n_slots * self.qpk * hd
+            N.check(N.lib.fs_kv_write(
+                N.ptr(self.cache.pool), N.ptr(self.cache.block_table), self.cache.pages_per_seq,
+                plan.ptr("tok_seq", a), plan.ptr("tok_pos", a), plan.ptr("tok_src", a), b - a,
+                N.C.c_void_p(qkv.data_ptr() + 2 * qw),
+                N.C.c_void_p(qkv.data_ptr() + 2 * (qw + self.n_slots * hd)), hd, _stream()),
+                "fs_kv_write")
+        o.zero_()  # replicated slots of requests routed elsewhere stay 0
+        pf = plan.prefill[layer]
+        if pf is not None:                                               # K8
+            pf(qkv, self.row_width, o, o.shape[1])
+        d = plan._descs[layer]
+        if d is not None:                                                # K1
+            N.check(N.lib.fs_decode_attention(N.C.byref(d), _stream()), "fs_decode_attention")
+
+    def serve_attention_partial(self, layer: int, plan: StepPlan) -> torch.Tensor:
+        """This rank's pre-exchange attention contribution ``o @ Wo_g``."""
+        self._attention(layer, plan)
+        T = plan.T
+        torch.matmul(self.o_s[:T], self.wo[layer], out=self.part_s[:T])
+        return self.part_s[:T]
+
+    def serve_mlp_partial(self, layer: int, plan: StepPlan) -> torch.Tensor:
+        T = plan.T
+        if not len(self.ffn_cols):
+            return self.part_s[:T].zero_()
+        C = len(self.ffn_cols)
+        torch.matmul(self.x_s[:T], self.w_gu[layer], out=self.h_s[:T])
+        N.check(N.lib.fs_swiglu(N.ptr(self.h_s), T, C, 2 * C, N.ptr(self.act_s), C, _stream()),
+                "fs_swiglu")
+        torch.matmul(self.act_s[:T], self.w_d[layer], out=self.part_s[:T])
+        return self.part_s[:T]
+
+    def serve(self, plan: StepPlan, x: torch.Tensor = None) -> torch.Tensor:
+        """Run one iteration: ``x`` [T, hidden] (device or pinned host; None
+        = the resident ``x_s``) -> the updated residual stream [T, hidden]."""
+        T = plan.T
+        xs = self.x_s[:T]
+        if x is not None:
+            xs.copy_(x, non_blocking=True)
+        for layer in range(self.model.num_layers):
+            part = self.serve_attention_partial(layer, plan)
+            if self.group is not None:
+                torch.distributed.all_reduce(part, group=self.group)
+            xs.add_(part)
+            if self.mlp:
+                part = self.serve_mlp_partial(layer, plan)
+                if self.group is not None:
+                    torch.distributed.all_reduce(part, group=self.group)
+                xs.add_(part)
+        return xs
+
+    def serve_launches(self, plan: StepPlan) -> int:
+        """Our kernel launches per iteration (K3 + K8 (+combine) + K1 per
+        layer, swiglu per layer with the MLP)."""
+        n = 0
+        for layer in range(self.model.num_layers):
+            n += plan.kv_seg[layer + 1] > plan.kv_seg[layer]
+            pf = plan.prefill[layer]
+            n += 0 if pf is None else 1 + (pf.n_comb > 0)
+            n += plan._descs[layer] is not None
+            n += bool(self.mlp and len(self.ffn_cols))
+        return int(n)
+
+
+def emulated_serving_step(ranks, plans, x: torch.Tensor) -> torch.Tensor:
+    """Single-process emulation of one iteration over several ranks on one
+    GPU: per layer each rank's partial, summed in ascending rank order in
+    fp32 (refexec.py:283-307), then the residual."""
+    order = sorted(range(len(ranks)), key=lambda i: ranks[i].rank)
+    x = x.to(torch.bfloat16)
+    T = x.shape[0]
+    model = ranks[0].model
+    for layer in range(model.num_layers):
+        for fn in ("serve_attention_partial", "serve_mlp_partial"):
+            if fn == "serve_mlp_partial" and not ranks[0].mlp:
+                continue
+            total = None
+            for i in order:
+                ranks[i].x_s[:T].copy_(x)
+                part = getattr(ranks[i], fn)(layer, plans[i]).float()
+                total = part if total is None else total + part
+            x = x + total.to(torch.bfloat16)
+    return x
