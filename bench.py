@@ -21,6 +21,9 @@ At N=1 the line also carries (rank 0 only):
 * ``failure_states`` -- BASELINE config 3 (Llama-3-70B-shaped, B=64,
   ctx 4096) at the 8 -> 7 -> 6 -> 5 on-demand shrink chain, every rank of
   every world emulated on this GPU (exchange excluded: one GPU);
+* ``mixed_trace`` -- config 5: mixed prefill/decode iterations (Alg. 1
+  chunked prefill + decode, 32k prompts) on the 7 survivors, every rank
+  emulated on this GPU;
 * ``recovery`` -- config 4 microbenchmark (KV restore from the pinned host
   backup, weight shards) after 1-3 losses;
 * ``cpu_baseline`` -- the CPU oracle port on a bounded sample.
@@ -245,6 +248,115 @@ def failure_states(steps, warmup, config, batch=64, ctx=4096, fails=(7, 3, 5), m
     return out
 
 
+# ------------------------------------------------- mixed trace (config 5) --
+def sharegpt_trace(n=120, seed=20240701, n_long=2, long_len=32768):
+    """ShareGPT-shaped lognormal lengths (the reference's synth_trace
+    recipe, traces.py:66-84: median 256 / sigma 1.0 inputs, median 192 /
+    sigma 0.8 outputs) with ``n_long`` injected 32k-token prompts."""
+    import math
+    import random
+    rng = random.Random(seed)
+
+    def ln(median, sigma, mx):
+        return max(1, min(int(round(math.exp(math.log(median) + sigma * rng.gauss(0, 1)))), mx))
+
+    rows = [(ln(256.0, 1.0, 8192), ln(192.0, 0.8, 2048)) for _ in range(n)]
+    for i in range(n_long):
+        rows.insert((i + 1) * n // (n_long + 1), (long_len, ln(192.0, 0.8, 2048)))
+    return rows
+
+
+def mixed_iterations(inputs, ranks, budget, skip, n_iter):
+    """Router + Alg. 1 batcher over the trace (all requests queued at t=0);
+    the first ``skip`` iterations only advance the host state (their KV is
+    random-filled), the next ``n_iter`` are returned as StepBatches."""
+    from paper_2511_14116_b200.core import Request
+    from paper_2511_14116_b200.scheduler import (SchedulerState, build_prefill_batch,
+                                                 route_request)
+    from paper_2511_14116_b200.serving import StepBatch
+    st = SchedulerState(token_budget=budget, rank_set=tuple(ranks))
+    reqs = [Request(id=i, arrival_time=0.0, input_len=a, output_len=o)
+            for i, (a, o) in enumerate(inputs)]
+    routing = {r.id: route_request(st, r) for r in reqs}
+    steps = []
+    for it in range(skip + n_iter):
+        b = build_prefill_batch(st)
+        dec = [(r.id, r.input_len + r.tokens_decoded - 1) for r in reqs
+               if r.tokens_prefilled == r.input_len and 1 <= r.tokens_decoded < r.output_len]
+        if it >= skip:
+            steps.append(StepBatch(prefill=list(b.entries), decode=dec))
+        for rid, _, n in b.entries:
+            reqs[rid].tokens_prefilled += n
+        for rid, _ in dec:
+            reqs[rid].tokens_decoded += 1
+            st.note_decode_token(reqs[rid], routing[rid])
+        for r in reqs:
+            if r.tokens_prefilled == r.input_len and r.tokens_decoded == 0:
+                r.tokens_decoded = 1
+    caps = [a + o - 1 for a, o in inputs]
+    return routing, steps, caps
+
+
+def mixed_trace(skip=24, n_iter=3, budget=2048, fail=7):
+    """BASELINE config 5: Llama-3-70B-shaped mixed prefill/decode iterations
+    of a ShareGPT-shaped trace with two 32k prompts, load-aware routing and
+    Alg. 1 chunked prefill on the 7 survivors of hybrid(8) after losing GPU
+    ``fail`` (on-demand target).  Every rank timed on this GPU."""
+    import torch
+    from paper_2511_14116_b200.placement import make_placement, owner_array
+    from paper_2511_14116_b200.recovery import plan_weight_recovery
+    from paper_2511_14116_b200.serving import HybridServingRank
+    model = llama70b()
+    plan = make_placement("hybrid", model, range(8))
+    alive = [g for g in range(8) if g != fail]
+    plan = plan_weight_recovery(model, plan, alive, "on_demand").target_plan("hybrid", model)
+    owner = owner_array(plan, model.num_kv_heads)
+    shards = [plan.ffn.owner[s] for s in range(plan.ffn.num_shards)]
+    inputs = sharegpt_trace()
+    routing, steps, caps = mixed_iterations(inputs, alive, budget, skip, n_iter)
+    max_tokens = max(s.num_tokens for s in steps)
+    per_rank = []
+    for g in alive:
+        eng = HybridServingRank(model, owner, g, routing, caps, max_tokens, seed=0,
+                                shard_owner=shards)
+        eng.fill_random_kv(100 + g)
+        t0 = time.perf_counter()
+        plans = [eng.plan(s) for s in steps]
+        plan_ms = (time.perf_counter() - t0) * 1e3 / len(plans)
+        xs = [torch.randn((s.num_tokens, model.hidden_dim), device="cuda").to(torch.bfloat16)
+              for s in steps]
+        eng.serve(plans[0], xs[0])  # warm-up (cuBLAS heuristics, attributes)
+        torch.cuda.synchronize()
+        times = []
+        for p, x in zip(plans, xs):
+            s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s_.record()
+            eng.serve(p, x)
+            e_.record()
+            torch.cuda.synchronize()
+            times.append(s_.elapsed_time(e_))
+        per_rank.append({"rank": g, "iter_ms": [round(t, 3) for t in times],
+                         "host_plan_ms": round(plan_ms, 2),
+                         "kv_read_gb": [round(p.kv_read_bytes / 1e9, 3) for p in plans],
+                         "prefill_attn_tflop": [round(p.attn_flops / 1e12, 3) for p in plans],
+                         "launches": [eng.serve_launches(p) for p in plans]})
+        del eng, plans
+        torch.cuda.empty_cache()
+    it_ms = [max(r["iter_ms"][i] for r in per_rank) for i in range(len(steps))]
+    toks = [s.num_tokens for s in steps]
+    return {"workload": "C5 Llama-3-70B-shaped mixed prefill/decode iterations (attention + TP "
+                        "MLP), ShareGPT-shaped trace (120 requests) + two 32k prompts, "
+                        f"load-aware routing + Alg. 1 chunked prefill (budget {budget}) on 7 "
+                        f"survivors (hybrid(8), GPU {fail} lost, on-demand target)",
+            "emulation": "every rank timed on this one GPU; iteration = max over ranks; NCCL "
+                         "exchange excluded (1 GPU)",
+            "iterations": [{"prefill_tokens": sum(n for _, _, n in s.prefill),
+                            "prefill_chunks": len(s.prefill), "decode_tokens": len(s.decode),
+                            "max_rank_ms": round(t, 3)} for s, t in zip(steps, it_ms)],
+            "tok_s": round(sum(toks) / (sum(it_ms) / 1e3), 1),
+            "ranks": per_rank}
+
+
 # ------------------------------------------------------------ CPU oracle --
 def cpu_oracle_rate(qpk, ctx, seconds=8.0):
     """Items/s of the oracle port (float64 numpy decode of one (kv head,
@@ -438,6 +550,8 @@ def run_ours(args, world, rank, local_rank):
         if not args.skip_failure_states:
             line["failure_states"] = failure_states(args.steps, args.warmup, args.kernel_config,
                                                     mlp=not args.no_mlp)
+        if not args.skip_mixed:
+            line["mixed_trace"] = mixed_trace()
         if not args.skip_recovery:
             try:
                 from paper_2511_14116_b200.recovery_exec import recovery_microbench
@@ -467,6 +581,8 @@ def main():
     ap.add_argument("--kernel-config", type=int, default=0)
     ap.add_argument("--skip-failure-states", action="store_true")
     ap.add_argument("--skip-recovery", action="store_true")
+    ap.add_argument("--skip-mixed", action="store_true",
+                    help="skip the config-5 mixed prefill/decode trace section")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--gemm", default="cublas", choices=("cublas", "tcgen05"))
     ap.add_argument("--no-mlp", action="store_true",

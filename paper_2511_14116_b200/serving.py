@@ -36,7 +36,7 @@ import torch
 from . import _native as N
 from .core import ValidationError
 from .hybrid import HybridDecodeRank
-from .prefill import PrefillLaunch
+from .prefill import PrefillLaunch, PrefillTilePlan
 
 
 @dataclass
@@ -54,72 +54,94 @@ class StepBatch:
 
 
 class StepPlan:
-    """Device work tables of one iteration on one rank (all layers)."""
+    """Device work tables of one iteration on one rank (all layers), built
+    with vectorised numpy and uploaded in ONE host->device copy; the K8 tile
+    plans are shared by the layers with the same item structure."""
 
     def __init__(self, eng: "HybridServingRank", batch: StepBatch):
         self.batch = batch
         T = batch.num_tokens
         if T > eng.max_tokens:
             raise ValidationError(f"iteration has {T} tokens > max_tokens {eng.max_tokens}")
-        for r, s, n in batch.prefill:
-            if n < 1 or s < 0 or s + n > eng.request_capacity[r]:
-                raise ValidationError(f"prefill chunk {(r, s, n)} outside request capacity")
-        for r, pos in batch.decode:
-            if pos < 0 or pos + 1 > eng.request_capacity[r]:
-                raise ValidationError(f"decode token {(r, pos)} outside request capacity")
+        cap = eng.request_capacity
+        E = np.array(batch.prefill, dtype=np.int64).reshape(-1, 3)
+        D = np.array(batch.decode, dtype=np.int64).reshape(-1, 2)
+        e_req, e_st, e_len = E[:, 0], E[:, 1], E[:, 2]
+        d_req, d_pos = D[:, 0], D[:, 1]
+        if E.size and (e_len.min() < 1 or e_st.min() < 0 or np.any(e_st + e_len > cap[e_req])):
+            raise ValidationError("a prefill chunk lies outside its request's capacity")
+        if D.size and (d_pos.min() < 0 or np.any(d_pos + 1 > cap[d_req])):
+            raise ValidationError("a decode token lies outside its request's capacity")
         self.T = T
-        L, S, qpk, hd = eng.model.num_layers, eng.n_slots, eng.qpk, eng.model.head_dim
-        rw, ow = eng.row_width, S * qpk * hd
-        pre_row = np.cumsum([0] + [n for _, _, n in batch.prefill])[:-1]
-        Tp = int(sum(n for _, _, n in batch.prefill))
+        L, qpk, hd = eng.model.num_layers, eng.qpk, eng.model.head_dim
+        rw, ow = eng.row_width, eng.n_slots * qpk * hd
+        rpt = rw // hd  # 128-element rows per token row of qkv
+        Tp = int(e_len.sum())
+        e_row = np.concatenate([[0], np.cumsum(e_len)[:-1]]).astype(np.int64) if E.size \
+            else np.zeros(0, np.int64)
+        d_row = Tp + np.arange(D.shape[0], dtype=np.int64)
         tok_seq, tok_pos, tok_src, kv_seg = [], [], [], [0]
         dec = {k: [] for k in ("seq", "len", "qoff", "ooff")}
         dec_seg = [0]
         self.prefill = []
+        tile_plans = {}
+        target = 4 * N.lib.fs_device_sms(eng.cache.dev_index)
+        n_kv = n_dec = 0
         for layer in range(L):
             idx = eng.item_index[layer]
             pf = {k: [] for k in ("seq", "start", "len", "qoff", "ooff")}
             for j in range(len(eng.work.slot_heads[layer])):
-                for e, (r, st, n) in enumerate(batch.prefill):
-                    it = int(idx[j, r])
-                    if it < 0:
-                        continue  # replicated head, request routed elsewhere
-                    row = int(pre_row[e])
-                    pf["seq"].append(it)
+                if E.size:
+                    it = idx[j, e_req]
+                    m = it >= 0  # replicated head: only requests routed here
+                    seq, st, ln, row = it[m], e_st[m], e_len[m], e_row[m]
+                    pf["seq"].append(seq)
                     pf["start"].append(st)
-                    pf["len"].append(n)
+                    pf["len"].append(ln)
                     pf["qoff"].append(row * rw + j * qpk * hd)
                     pf["ooff"].append(row * ow + j * qpk * hd)
-                    tok_seq.append(np.full(n, it))
-                    tok_pos.append(np.arange(st, st + n))
-                    tok_src.append((row + np.arange(n)) * (rw // hd) + j)
-                for d, (r, pos) in enumerate(batch.decode):
-                    it = int(idx[j, r])
-                    if it < 0:
-                        continue
-                    row = Tp + d
-                    dec["seq"].append(it)
-                    dec["len"].append(pos + 1)
-                    dec["qoff"].append(row * rw + j * qpk * hd)
-                    dec["ooff"].append(row * ow + j * qpk * hd)
-                    tok_seq.append(np.array([it]))
-                    tok_pos.append(np.array([pos]))
-                    tok_src.append(np.array([row * (rw // hd) + j]))
-            kv_seg.append(sum(a.size for a in tok_seq))
-            dec_seg.append(len(dec["seq"]))
-            self.prefill.append(PrefillLaunch(eng.cache, pf["seq"], pf["start"], pf["len"],
-                                              pf["qoff"], pf["ooff"]) if pf["seq"] else None)
+                    rep = np.repeat(np.arange(seq.size), ln)
+                    local = np.arange(rep.size) - np.repeat(np.cumsum(ln) - ln, ln)
+                    tok_seq.append(seq[rep])
+                    tok_pos.append(st[rep] + local)
+                    tok_src.append((row[rep] + local) * rpt + j)
+                    n_kv += rep.size
+                if D.size:
+                    it = idx[j, d_req]
+                    m = it >= 0
+                    dec["seq"].append(it[m])
+                    dec["len"].append(d_pos[m] + 1)
+                    dec["qoff"].append(d_row[m] * rw + j * qpk * hd)
+                    dec["ooff"].append(d_row[m] * ow + j * qpk * hd)
+                    tok_seq.append(it[m])
+                    tok_pos.append(d_pos[m])
+                    tok_src.append(d_row[m] * rpt + j)
+                    n_kv += int(m.sum())
+                    n_dec += int(m.sum())
+            kv_seg.append(n_kv)
+            dec_seg.append(n_dec)
+            launch = None
+            if pf["seq"] and sum(a.size for a in pf["seq"]):
+                cols = {k: np.concatenate(v) for k, v in pf.items()}
+                key = (cols["start"].tobytes(), cols["len"].tobytes())
+                tp = tile_plans.get(key)
+                if tp is None:
+                    tp = tile_plans[key] = PrefillTilePlan(cols["start"], cols["len"], qpk, target)
+                launch = PrefillLaunch(eng.cache, cols["seq"], cols["start"], cols["len"],
+                                       cols["qoff"], cols["ooff"], tile_plan=tp, upload=False)
+            self.prefill.append(launch)
         cat = (lambda xs: np.concatenate(xs).astype(np.int32) if xs else np.zeros(0, np.int32))
-        n_kv = kv_seg[-1]
-        n_dec = dec_seg[-1]
         self.kv_seg = kv_seg
         self.dec_seg = np.array(dec_seg, dtype=np.int32)
-        flat = np.concatenate([cat(tok_seq), cat(tok_pos), cat(tok_src),
-                               np.array(dec["seq"], np.int32), np.array(dec["len"], np.int32),
-                               np.array(dec["qoff"], np.int32), np.array(dec["ooff"], np.int32),
-                               self.dec_seg])
+        d_len = cat(dec["len"])
+        parts = [cat(tok_seq), cat(tok_pos), cat(tok_src), cat(dec["seq"]), d_len,
+                 cat(dec["qoff"]), cat(dec["ooff"]), self.dec_seg]
+        pf_base = sum(x.size for x in parts)
+        for lp in self.prefill:
+            if lp is not None:
+                parts.append(lp.host_table)
         dev = eng.device
-        self._tab = torch.from_numpy(flat).to(dev)
+        self._tab = torch.from_numpy(np.concatenate(parts)).to(dev)
         o = 0
         self._off = {}
         for name, size in (("tok_seq", n_kv), ("tok_pos", n_kv), ("tok_src", n_kv),
@@ -127,6 +149,14 @@ class StepPlan:
                            ("d_ooff", n_dec), ("d_seg", L + 1)):
             self._off[name] = o
             o += size
+        slots = max([lp.n_slots for lp in self.prefill if lp is not None] + [0])
+        self.pf_part_o = torch.empty((max(1, slots), 64, hd), dtype=torch.float32, device=dev)
+        self.pf_part_lse = torch.empty((max(1, slots), 64), dtype=torch.float32, device=dev)
+        o = pf_base
+        for lp in self.prefill:
+            if lp is not None:
+                lp.bind(self._tab, o, self.pf_part_o, self.pf_part_lse)
+                o += lp.host_table.size
         self.n_dec = n_dec
         self.dec_sem = torch.zeros(max(1, n_dec), dtype=torch.int32, device=dev)
         self.page_off = torch.zeros(n_dec + L, dtype=torch.int32, device=dev)
@@ -137,7 +167,7 @@ class StepPlan:
         # algorithmic KV bytes of the iteration on this rank (512 B per
         # (head, token) read: decode items read len, prefill tiles their
         # causal page range)
-        self.kv_read_bytes = 512 * int(np.sum(dec["len"])) + sum(
+        self.kv_read_bytes = 512 * int(d_len.astype(np.int64).sum()) + sum(
             (p.kv_page_reads * N.PAGE_BYTES) for p in self.prefill if p is not None)
         self.attn_flops = sum(p.flops for p in self.prefill if p is not None)
 
