@@ -186,6 +186,7 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) decode_kernel(const DecodePa
     const int64_t W = p.n_warps;
     const int64_t w = (int64_t)blockIdx.x * WARPS + warp;
     const int64_t x0 = w * P / W, x1 = (w + 1) * P / W;
+    grid_launch_dependents();  // the next launch may stage its pages early
     if (x0 >= x1) return;  // warp-uniform; no CTA-wide barriers below
 
     const uint32_t sbase = smem_u32(smem);

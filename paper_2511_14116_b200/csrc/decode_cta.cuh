@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_cta_kernel(const DecodeP
     const int64_t C = p.n_warps;  // partition units = CTAs
     const int64_t c = blockIdx.x;
     const int64_t x0 = c * P / C, x1 = (c + 1) * P / C;
+    grid_launch_dependents();  // the next launch may stage its pages early
     if (x0 >= x1) return;  // CTA-uniform
 
     const uint32_t sbase = smem_u32(smem);
@@ -282,41 +283,103 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_cta_kernel(const DecodeP
                 for (int64_t s = clo; s <= chi; ++s) nseg += warp_live(s, C, P);
             }
             if (s_prev == nseg - 1) {
+                // last CTA of the item: merge its (up to ~all-CTA) partials
+                // with every warp -- warp w takes segments clo+w, clo+w+WARPS,
+                // ... for all queries (8 independent float4 loads per
+                // segment), then the warps' sums are reduced in smem.  A
+                // one-warp serial merge costs ~40 us when one long item
+                // spans all 148 CTAs (batch-1 decode).
                 __threadfence();
                 const bool all_live = P >= C;
-                for (int q = warp; q < p.qpk; q += WARPS) {
-                    float M = -INFINITY;
-                    for (int64_t k = lane; k <= chi - clo; k += 32) {
-                        const int64_t s = clo + k;
-                        if (all_live || warp_live(s, C, P))
-                            M = fmaxf(M, __ldcg(p.part_lse + (item + s) * p.qpk + q));
-                    }
+                const int qpk = p.qpk;
+                float mx[FS_MAX_Q_PER_KV];
+#pragma unroll
+                for (int q = 0; q < FS_MAX_Q_PER_KV; ++q) mx[q] = -INFINITY;
+                for (int64_t s = clo + threadIdx.x; s <= chi; s += NT) {
+                    if (!all_live && !warp_live(s, C, P)) continue;
+#pragma unroll
+                    for (int q = 0; q < FS_MAX_Q_PER_KV; ++q)
+                        if (q < qpk) mx[q] = fmaxf(mx[q], __ldcg(p.part_lse + (item + s) * qpk + q));
+                }
+                float *slot = merge + warp * kSlot;
+#pragma unroll
+                for (int q = 0; q < FS_MAX_Q_PER_KV; ++q) {
 #pragma unroll
                     for (int sh = 1; sh < 32; sh <<= 1)
-                        M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, sh));
+                        mx[q] = fmaxf(mx[q], __shfl_xor_sync(0xffffffffu, mx[q], sh));
+                    if (lane == 0) slot[q] = mx[q];
+                }
+                named_bar(1, NT);
+#pragma unroll
+                for (int q = 0; q < FS_MAX_Q_PER_KV; ++q) {
+                    float m = -INFINITY;
+#pragma unroll
+                    for (int k = 0; k < WARPS; ++k) m = fmaxf(m, merge[k * kSlot + q]);
+                    mx[q] = m;
+                }
+                float lw[FS_MAX_Q_PER_KV];
+                float4 acc[FS_MAX_Q_PER_KV];
+#pragma unroll
+                for (int q = 0; q < FS_MAX_Q_PER_KV; ++q) {
+                    lw[q] = 0.f;
+                    acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+                for (int64_t s = clo + warp; s <= chi; s += WARPS) {
+                    if (!all_live && !warp_live(s, C, P)) continue;
+                    const float *ls = p.part_lse + (item + s) * qpk;
+                    const float4 *os = reinterpret_cast<const float4 *>(p.part_o + (item + s) * qpk * kHeadDim);
+                    float4 v[FS_MAX_Q_PER_KV];
+                    float wk[FS_MAX_Q_PER_KV];
+#pragma unroll
+                    for (int q = 0; q < FS_MAX_Q_PER_KV; ++q) {
+                        if (q < qpk) {
+                            wk[q] = __ldcg(ls + q);
+                            v[q] = __ldcg(os + q * (kHeadDim / 4) + lane);
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < FS_MAX_Q_PER_KV; ++q) {
+                        if (q < qpk) {
+                            const float w = fast_exp2(wk[q] - mx[q]);
+                            lw[q] += w;
+                            acc[q].x += w * v[q].x;
+                            acc[q].y += w * v[q].y;
+                            acc[q].z += w * v[q].z;
+                            acc[q].w += w * v[q].w;
+                        }
+                    }
+                }
+                named_bar(1, NT);  // everyone has read the maxima
+                float *om = slot + 2 * FS_MAX_Q_PER_KV;
+#pragma unroll
+                for (int q = 0; q < FS_MAX_Q_PER_KV; ++q) {
+                    if (q < qpk) {
+                        if (lane == 0) slot[FS_MAX_Q_PER_KV + q] = lw[q];
+                        *reinterpret_cast<float4 *>(om + q * kMergeStride + lane * 4) = acc[q];
+                    }
+                }
+                named_bar(1, NT);
+                for (int q = warp; q < qpk; q += WARPS) {
                     float L = 0.f;
-                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 4
-                    for (int64_t s = clo; s <= chi; ++s) {
-                        if (!all_live && !warp_live(s, C, P)) continue;
-                        const float wk = fast_exp2(__ldcg(p.part_lse + (item + s) * p.qpk + q) - M);
-                        const float4 v = __ldcg(reinterpret_cast<const float4 *>(
-                                                    p.part_o + ((item + s) * p.qpk + q) * kHeadDim) +
-                                                lane);
-                        L += wk;
-                        acc.x += wk * v.x;
-                        acc.y += wk * v.y;
-                        acc.z += wk * v.z;
-                        acc.w += wk * v.w;
+                    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                    for (int k = 0; k < WARPS; ++k) {
+                        L += merge[k * kSlot + FS_MAX_Q_PER_KV + q];
+                        const float4 t = *reinterpret_cast<const float4 *>(
+                            merge + k * kSlot + 2 * FS_MAX_Q_PER_KV + q * kMergeStride + lane * 4);
+                        sum.x += t.x;
+                        sum.y += t.y;
+                        sum.z += t.z;
+                        sum.w += t.w;
                     }
                     const float inv = 1.f / L;
                     const int64_t ob = (int64_t)p.item_ooff[item] + q * kHeadDim + lane * 4;
                     if (p.out_fp32) {
                         *reinterpret_cast<float4 *>(static_cast<float *>(p.out) + ob) =
-                            make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+                            make_float4(sum.x * inv, sum.y * inv, sum.z * inv, sum.w * inv);
                     } else {
-                        __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
-                        __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+                        __nv_bfloat162 lo = __floats2bfloat162_rn(sum.x * inv, sum.y * inv);
+                        __nv_bfloat162 hi = __floats2bfloat162_rn(sum.z * inv, sum.w * inv);
                         uint2 pk;
                         pk.x = *reinterpret_cast<uint32_t *>(&lo);
                         pk.y = *reinterpret_cast<uint32_t *>(&hi);
