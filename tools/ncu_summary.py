@@ -24,7 +24,7 @@ import shutil
 import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-STEP_KERNELS = ("decode_kernel", "nvjet", "gemm", "cutlass", "bfloat16_copy", "plan_pages")
+STEP_KERNELS = ("decode", "nvjet", "gemm", "cutlass", "bfloat16_copy", "plan_pages", "swiglu")
 
 
 def launch_table(path):
@@ -69,7 +69,7 @@ def main():
         step_t = sum(t for _, t in step.values())
         lines = [f"# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache,"
                  f" serialised) of: python bench.py --steps 3 --warmup 3 --skip-failure-states"
-                 f" --skip-recovery --skip-cpu", "",
+                 f" --skip-recovery --skip-cpu --skip-mixed", "",
                  "## step kernels (share of the decode-step kernels)",
                  f"{'launches':>8} {'total_us':>12} {'avg_us':>10} {'share':>7}  kernel"]
         for k, (c, t) in sorted(step.items(), key=lambda x: -x[1][1]):
@@ -102,7 +102,7 @@ def main():
         tot_st = sum(stalls.values()) or 1.0
         summ = {
             "source": f"profiles/{tag}_decode_full.ncu-rep (ncu --set full --clock-control none"
-                      " -k regex:decode_kernel -s 40 -c 1, bench.py C2 config)",
+                      " -k regex:decode -s 40 -c 1, bench.py C2 config)",
             "kernel": m.get("Kernel Name", ("decode_kernel", ""))[0],
             "duration_us": dur * 1e6,
             "dram_bytes_read": rd, "dram_bytes_write": wr,
@@ -124,6 +124,40 @@ def main():
         with open(os.path.join(prof, "ncu_decode_summary.json"), "w") as fh:
             json.dump(summ, fh, indent=1)
         shutil.copy(rep, os.path.join(prof, f"{tag}_decode_full.ncu-rep"))
+        print(json.dumps(summ, indent=1))
+    rep = os.path.join(a.src, "prefill_full.ncu-rep")
+    if os.path.exists(rep):
+        m = raw_metrics(rep)
+
+        def num2(k):
+            v, u = m[k]
+            f = float(v.replace(",", ""))
+            return f * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "us": 1e-6, "ms": 1e-3,
+                        "ns": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "nsecond": 1e-9}.get(u, 1.0)
+        dur = num2("gpu__time_duration.sum")
+        # tools/prefill_bench.py --cases 1x2048@8192 (q_per_kv 8): 2048 chunk
+        # tokens behind an 8192-token prefix, 4*hd FLOP per (q head, key)
+        vis = 8192 * 2048 + 2048 * 2049 // 2
+        flops = 4 * 128 * 8 * vis
+        summ = {
+            "source": f"profiles/{tag}_prefill_full.ncu-rep (ncu --set full --clock-control none "
+                      "-k regex:prefill_kernel -s 2 -c 1, tools/prefill_bench.py --cases "
+                      "1x2048@8192)",
+            "kernel": m.get("Kernel Name", ("prefill_kernel", ""))[0],
+            "duration_us": dur * 1e6,
+            "algorithmic_flop": flops,
+            "achieved_tflops_under_ncu": flops / dur / 1e12,
+            "dram_bytes": num2("dram__bytes_read.sum") + num2("dram__bytes_write.sum"),
+            "registers_per_thread": int(float(m["launch__registers_per_thread"][0])),
+            "grid": int(float(m["launch__grid_size"][0])),
+            "block": int(float(m["launch__block_size"][0])),
+            "tensor_pipe_pct": float(
+                m["sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"][0]),
+            "sm_active_over_elapsed": num2("sm__cycles_active.avg") / num2("sm__cycles_elapsed.avg"),
+        }
+        with open(os.path.join(prof, "ncu_prefill_summary.json"), "w") as fh:
+            json.dump(summ, fh, indent=1)
+        shutil.copy(rep, os.path.join(prof, f"{tag}_prefill_full.ncu-rep"))
         print(json.dumps(summ, indent=1))
 
 
