@@ -68,9 +68,11 @@ extern "C" {
 #define FS_MODE_HYBRID 2
 
 /* Page format: one page holds FS_PAGE_TOKENS tokens of ONE kv head:
- * K rows [0,16) then V rows [0,16), each row FS_HEAD_DIM bf16 (256 B), the
- * 16-byte chunk c of row r stored at chunk position c ^ (r & 7) (bank-
- * conflict-free ldmatrix after a linear TMA bulk copy).  8 KiB per page. */
+ * K rows [0,16) then V rows [0,16).  Each half is two 2 KB atoms (head
+ * dims 0-63, then 64-127); an atom is 16 rows x 128 B with the 16-byte chunk
+ * c (0..7) of row r stored at chunk position c ^ (r & 7) -- the tcgen05 /
+ * TMA SWIZZLE_128B pattern, and bank-conflict-free for ldmatrix.  8 KiB per
+ * page. */
 #define FS_PAGE_TOKENS 16
 #define FS_HEAD_DIM 128
 #define FS_PAGE_BYTES 8192

@@ -32,11 +32,15 @@ constexpr int kPageTokens = FS_PAGE_TOKENS;
 constexpr int kHeadDim = FS_HEAD_DIM;
 constexpr int kPageBytes = FS_PAGE_BYTES;
 constexpr int kHalfPage = FS_PAGE_BYTES / 2;   // K rows, then V rows
-constexpr int kRowBytes = FS_HEAD_DIM * 2;      // 256 B per token row
 
-// byte offset of 16-byte chunk `c` (0..15) of row `r` inside a K or V half
+// byte offset of 16-byte chunk `c` (0..15) of row `r` inside a K or V half:
+// two 2 KB atoms (dims 0-63, 64-127), each 16 rows x 128 B with the 128 B
+// swizzle (chunk c&7 of row r at c&7 ^ r&7).  Each atom is a UMMA-canonical
+// SWIZZLE_128B block, so pages TMA'd atom by atom into consecutive smem
+// rows are tcgen05 operands as is; ldmatrix over 8 rows stays conflict-free.
+constexpr int kAtomBytes = 2048;
 __host__ __device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t c) {
-    return r * kRowBytes + ((c ^ (r & 7u)) << 4);
+    return ((c >> 3) * kAtomBytes) + r * 128 + (((c & 7u) ^ (r & 7u)) << 4);
 }
 
 int sm_count(int device);

@@ -281,8 +281,9 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) decode_kernel(const DecodePa
             if (tail) {
                 // rows >= valid may hold stale bytes; zero the V rows so
                 // 0-probability tokens cannot inject NaN/Inf into P.V
-                for (int c = valid * 16 + lane; c < kPageTokens * 16; c += 32)
-                    reinterpret_cast<uint4 *>(page_s + kHalfPage)[c] = make_uint4(0, 0, 0, 0);
+                for (int c = valid * 8 + lane; c < kPageTokens * 16; c += 32)
+                    if ((c & 127) >= valid * 8)  // both atoms: rows >= valid
+                        reinterpret_cast<uint4 *>(page_s + kHalfPage)[c] = make_uint4(0, 0, 0, 0);
             }
             if (append) {
                 // fused K3: the new token (position len-1) from the

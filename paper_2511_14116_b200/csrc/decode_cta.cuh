@@ -128,8 +128,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_cta_kernel(const DecodeP
             if (tail | append) {
                 uint8_t *page_s = smem + (kb - sbase);
                 if (tail)
-                    for (int cc = valid * 16 + lane; cc < kPageTokens * 16; cc += 32)
-                        reinterpret_cast<uint4 *>(page_s + kHalfPage)[cc] = make_uint4(0, 0, 0, 0);
+                    for (int cc = valid * 8 + lane; cc < kPageTokens * 16; cc += 32)
+                        if ((cc & 127) >= valid * 8)  // both atoms: rows >= valid
+                            reinterpret_cast<uint4 *>(page_s + kHalfPage)[cc] = make_uint4(0, 0, 0, 0);
                 if (append) {
                     const uint32_t r = (len - 1) % kPageTokens, ch = lane & 15, half = lane >> 4;
                     const int64_t src = (half ? p.item_voff[item] : p.item_koff[item]) + ch * 8;

@@ -114,15 +114,16 @@ __global__ void __launch_bounds__((kConsumerWarps + 2) * 32) prefill_kernel(cons
             }
             const int s = k % STAGES;
             mbar_wait(full0 + 8 * s, (k / STAGES) & 1);
-            uint4 *vh = reinterpret_cast<uint4 *>(smem + s * kPageBytes + kHalfPage) + cw * 128;
+            // warp cw converts atom cw (dims 64cw..64cw+63) of the V half
+            uint4 *vh = reinterpret_cast<uint4 *>(smem + s * kPageBytes + kHalfPage + cw * kAtomBytes);
             // rows past the item's last written position may hold stale
             // bytes: zero them (their P is 0, but 0 * NaN/Inf is not)
-            const int rows_ok = kv_end - (pg0 + k) * kPageTokens - cw * 8;
+            const int rows_ok = kv_end - (pg0 + k) * kPageTokens;
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-                const int idx = c * 32 + lane;
+                const int idx = c * 32 + lane;  // row idx >> 3 of the atom
                 uint4 v = vh[idx];
-                if (rows_ok >= 8 || (idx >> 4) < rows_ok) {
+                if (rows_ok >= kPageTokens || (idx >> 3) < rows_ok) {
                     v.x = bf16x2_to_f16x2(v.x);
                     v.y = bf16x2_to_f16x2(v.y);
                     v.z = bf16x2_to_f16x2(v.z);

@@ -168,12 +168,13 @@ def test_kv_write_read_roundtrip_bitexact():
     cache.write_tokens(seq, pos, k, v)
     k2, v2 = cache.read_tokens(seq, pos)
     assert torch.equal(k, k2) and torch.equal(v, v2)
-    # the page format is swizzled: row r chunk c at c ^ (r & 7)
+    # the page format: K half = 2 atoms (dims 0-63, 64-127) x 16 rows x 8
+    # chunks, chunk c of row r at (c & 7) ^ (r & 7) of atom c >> 3
     page = cache.block_table[0, 0].item()
-    raw = cache.pool[page].view(torch.bfloat16)[: 16 * 128].view(16, 16, 8)
+    raw = cache.pool[page].view(torch.bfloat16)[: 16 * 128].view(2, 16, 8, 8)
     for r in (0, 5, 9):
-        for c in (0, 3, 15):
-            assert torch.equal(raw[r, c ^ (r & 7)], k[r, c * 8:(c + 1) * 8])
+        for c in (0, 3, 9, 15):
+            assert torch.equal(raw[c >> 3, r, (c & 7) ^ (r & 7)], k[r, c * 8:(c + 1) * 8])
 
 
 def test_plan_pages_matches_host_prefix():
