@@ -71,8 +71,10 @@ extern "C" {
  * K rows [0,16) then V rows [0,16).  Each half is two 2 KB atoms (head
  * dims 0-63, then 64-127); an atom is 16 rows x 128 B with the 16-byte chunk
  * c (0..7) of row r stored at chunk position c ^ (r & 7) -- the tcgen05 /
- * TMA SWIZZLE_128B pattern, and bank-conflict-free for ldmatrix.  8 KiB per
- * page. */
+ * TMA SWIZZLE_128B pattern, and bank-conflict-free for ldmatrix.  K is
+ * bf16; V is stored as f16 (fs_kv_write converts: exact for bf16 values
+ * with |v| in [2^-14, 65504], saturating beyond), so P.V runs with f16
+ * probabilities.  8 KiB per page. */
 #define FS_PAGE_TOKENS 16
 #define FS_HEAD_DIM 128
 #define FS_PAGE_BYTES 8192

@@ -2,6 +2,7 @@
 // wrappers (TMA bulk copy, mbarrier, ldmatrix, mma.sync, movmatrix).
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
@@ -187,6 +188,22 @@ __device__ __forceinline__ uint32_t bf16x2_to_f16x2(uint32_t v) {
         : "=r"(r)
         : "f"(__uint_as_float(v & 0xffff0000u)), "f"(__uint_as_float(v << 16)));
     return r;
+}
+
+// 8 bf16 -> 8 f16 (the V half of a page is stored in f16)
+__device__ __forceinline__ uint4 bf16x8_to_f16x8(uint4 v) {
+    v.x = bf16x2_to_f16x2(v.x);
+    v.y = bf16x2_to_f16x2(v.y);
+    v.z = bf16x2_to_f16x2(v.z);
+    v.w = bf16x2_to_f16x2(v.w);
+    return v;
+}
+
+// two f16 -> two bf16 (exact for values that came from bf16)
+__device__ __forceinline__ uint32_t f16x2_to_bf16x2(uint32_t v) {
+    __half2 h = *reinterpret_cast<__half2 *>(&v);
+    float2 f = __half22float2(h);
+    return pack_bf16(f.x, f.y);
 }
 #endif
 

@@ -15,11 +15,12 @@
 // pages that straddle the tile's diagonal.  The page layout (swizzled 16 B
 // chunks) is the one the decode kernel and the writers share.
 //
-// P.V runs in f16, not bf16: the producer warp converts each landed V half
-// page to f16 in place (exact for |v| in f16's normal range) and publishes
-// it on a third barrier, so the probabilities keep 11 mantissa bits -- bf16
-// P alone costs ~1.5e-3 mean relative error on long contexts, above the
-// 1e-3 the north star allows.
+// P.V runs in f16, not bf16: V pages are stored in f16 (exact for the bf16
+// values the projections produce, |v| <= 65504), so the probabilities keep
+// 11 mantissa bits -- bf16 P alone costs ~1.5e-3 mean relative error on long
+// contexts, above the 1e-3 the north star allows.  The producer warps zero
+// stale rows past an item's last token and publish each page on a third
+// barrier.
 //
 // Long causal ranges are split into page ranges (fs_plan_prefill_tiles) so
 // a handful of long requests still fill 148 SMs; split tiles write
@@ -114,24 +115,18 @@ __global__ void __launch_bounds__((kConsumerWarps + 2) * 32) prefill_kernel(cons
             }
             const int s = k % STAGES;
             mbar_wait(full0 + 8 * s, (k / STAGES) & 1);
-            // warp cw converts atom cw (dims 64cw..64cw+63) of the V half
-            uint4 *vh = reinterpret_cast<uint4 *>(smem + s * kPageBytes + kHalfPage + cw * kAtomBytes);
             // rows past the item's last written position may hold stale
-            // bytes: zero them (their P is 0, but 0 * NaN/Inf is not)
+            // bytes: zero them in this warp's atom (their P is 0, but 0 *
+            // NaN/Inf is not); V is already f16 in the pages
             const int rows_ok = kv_end - (pg0 + k) * kPageTokens;
+            if (rows_ok < kPageTokens) {
+                uint4 *vh = reinterpret_cast<uint4 *>(smem + s * kPageBytes + kHalfPage +
+                                                      cw * kAtomBytes);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int idx = c * 32 + lane;  // row idx >> 3 of the atom
-                uint4 v = vh[idx];
-                if (rows_ok >= kPageTokens || (idx >> 3) < rows_ok) {
-                    v.x = bf16x2_to_f16x2(v.x);
-                    v.y = bf16x2_to_f16x2(v.y);
-                    v.z = bf16x2_to_f16x2(v.z);
-                    v.w = bf16x2_to_f16x2(v.w);
-                } else {
-                    v = make_uint4(0, 0, 0, 0);
+                for (int c = 0; c < 4; ++c) {
+                    const int idx = c * 32 + lane;  // row idx >> 3 of the atom
+                    if ((idx >> 3) >= rows_ok) vh[idx] = make_uint4(0, 0, 0, 0);
                 }
-                vh[idx] = v;
             }
             // the stage is refilled by TMA (async proxy) later: order these
             // generic-proxy writes before it

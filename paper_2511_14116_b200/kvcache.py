@@ -138,7 +138,8 @@ class PagedKVCache:
         mask = cols[None, :] < seq_pages[:, None]
         bt[mask] = ids[:int(seq_pages.sum())]
         dev = self.device
-        self.pool = torch.empty((self.n_pages, N.PAGE_BYTES), dtype=torch.uint8, device=dev)
+        # zero-filled: unwritten rows hold finite values (0), never NaN bit patterns
+        self.pool = torch.zeros((self.n_pages, N.PAGE_BYTES), dtype=torch.uint8, device=dev)
         self.block_table = torch.from_numpy(bt.astype(np.int32)).to(dev)
         self.item_seq = torch.arange(n_seq, dtype=torch.int32, device=dev)
         self.item_len = torch.zeros(n_seq, dtype=torch.int32, device=dev)
