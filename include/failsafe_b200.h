@@ -166,8 +166,9 @@ int fs_decode_attention(const fs_decode_desc *d, void *stream);
  * .. item_start[i]+item_len[i]-1 of block-table row item_seq[i] (their K/V
  * already in the pages); chunk token j attends causally, including itself,
  * to positions 0..item_start[i]+j (refexec.py:92-97).  A tile = up to
- * fs_prefill_tokens_per_tile(q_per_kv) consecutive chunk tokens x all
- * q_per_kv heads (64 query rows) over the KV page range [page0, page1);
+ * fs_prefill_tokens_per_tile(q_per_kv, variant) consecutive chunk tokens x
+ * all q_per_kv heads (128 or 64 query rows) over the KV page range
+ * [page0, page1);
  * tile_slot < 0 -> the tile covers its whole causal range and writes the
  * output; otherwise it writes a partial (O/l, log2-sum-exp) to that slot and
  * the combine list merges slots comb_slot0 .. +comb_nsplit-1 of each
@@ -189,13 +190,16 @@ typedef struct fs_prefill_desc {
     int32_t n_comb;
     int32_t q_per_kv;          /* 1..8                                      */
     float scale;
-    float *part_o;             /* [partial_slots][64][128] fp32             */
-    float *part_lse;           /* [partial_slots][64]                       */
+    float *part_o;             /* [partial_slots][rows][128] fp32           */
+    float *part_lse;           /* [partial_slots][rows]                     */
     int64_t partial_slots;
+    int32_t variant;           /* 0: tcgen05 (TMEM accumulators, 128-row
+                                  tiles); 1: mma.sync (64-row tiles)        */
 } fs_prefill_desc;
 
-/* chunk tokens per 64-row prefill tile (64 / q_per_kv), or <0 */
-int fs_prefill_tokens_per_tile(int q_per_kv);
+/* chunk tokens per tile (rows / q_per_kv; rows = 128 for variant 0, 64 for
+ * variant 1), or <0 */
+int fs_prefill_tokens_per_tile(int q_per_kv, int variant);
 
 /* Host planner of the K8 launch: token tiles of every item, each split into
  * equal KV page ranges so the grid has >= ~target_units similar-sized
@@ -204,7 +208,7 @@ int fs_prefill_tokens_per_tile(int q_per_kv);
  * *n_tiles, combine groups in *n_comb and the partial slots used in
  * *n_slots.  FS_EVALIDATION if the arrays are too small. */
 int fs_plan_prefill_tiles(int32_t n_items, const int32_t *item_start, const int32_t *item_len,
-                          int32_t q_per_kv, int32_t target_units, int32_t max_tiles,
+                          int32_t q_per_kv, int32_t variant, int32_t target_units, int32_t max_tiles,
                           int32_t *tile_item, int32_t *tile_tok0, int32_t *tile_page0,
                           int32_t *tile_page1, int32_t *tile_slot, int32_t *n_tiles,
                           int32_t max_comb, int32_t *comb_item, int32_t *comb_tok0,

@@ -55,7 +55,7 @@ class PrefillDesc(C.Structure):
         ("comb_item", C.c_void_p), ("comb_tok0", C.c_void_p), ("comb_slot0", C.c_void_p),
         ("comb_nsplit", C.c_void_p), ("n_comb", C.c_int32), ("q_per_kv", C.c_int32),
         ("scale", C.c_float), ("part_o", C.c_void_p), ("part_lse", C.c_void_p),
-        ("partial_slots", C.c_int64),
+        ("partial_slots", C.c_int64), ("variant", C.c_int32),
     ]
 
 
@@ -73,8 +73,9 @@ _SIGS = {
     "fs_plan_pages": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
     "fs_decode_partial_slots": (C.c_int64, [C.c_int, C.c_int32, C.c_int32]),
     "fs_decode_attention": (C.c_int, [C.POINTER(DecodeDesc), C.c_void_p]),
-    "fs_prefill_tokens_per_tile": (C.c_int, [C.c_int]),
+    "fs_prefill_tokens_per_tile": (C.c_int, [C.c_int, C.c_int]),
     "fs_plan_prefill_tiles": (C.c_int, [C.c_int32, _i32p, _i32p, C.c_int32, C.c_int32, C.c_int32,
+                                        C.c_int32,
                                         _i32p, _i32p, _i32p, _i32p, _i32p, _i32p, C.c_int32,
                                         _i32p, _i32p, _i32p, _i32p, _i32p, _i32p]),
     "fs_prefill_attention": (C.c_int, [C.POINTER(PrefillDesc), C.c_void_p]),

@@ -52,6 +52,7 @@ struct PrefillParams {
     const int32_t *tile_item, *tile_tok0, *tile_page0, *tile_page1, *tile_slot;
     const int32_t *comb_item, *comb_tok0, *comb_slot0, *comb_nsplit;
     int32_t qpk, tpt;  // q heads per kv head, chunk tokens per tile
+    int32_t rows;      // query rows per tile (= partial rows per slot): 64 or 128
     float scale_log2;
     float *part_o, *part_lse;
 };
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 2) * 32) prefill_kernel(cons
 
 // merge the page-range splits of one (item, token tile): 4 threads per row,
 // 32 dims each, log-sum-exp weights in base 2
-__global__ void __launch_bounds__(256) prefill_combine_kernel(const PrefillParams p) {
+__global__ void __launch_bounds__(512) prefill_combine_kernel(const PrefillParams p) {
     const int g = blockIdx.x;
     const int item = p.comb_item[g], tok0 = p.comb_tok0[g];
     const int slot0 = p.comb_slot0[g], ns = p.comb_nsplit[g];
@@ -293,17 +294,17 @@ __global__ void __launch_bounds__(256) prefill_combine_kernel(const PrefillParam
     const int tok = tok0 + r / qpk, h = r % qpk;
     if (tok >= p.item_len[item]) return;
     float mx = -INFINITY;
-    for (int s = 0; s < ns; ++s) mx = fmaxf(mx, p.part_lse[(int64_t)(slot0 + s) * kTileRows + r]);
+    for (int s = 0; s < ns; ++s) mx = fmaxf(mx, p.part_lse[(int64_t)(slot0 + s) * p.rows + r]);
     float acc[32];
 #pragma unroll
     for (int d = 0; d < 32; ++d) acc[d] = 0.f;
     float den = 0.f;
     for (int s = 0; s < ns; ++s) {
-        const float lse = p.part_lse[(int64_t)(slot0 + s) * kTileRows + r];
+        const float lse = p.part_lse[(int64_t)(slot0 + s) * p.rows + r];
         const float w = lse == -INFINITY ? 0.f : fast_exp2(lse - mx);
         den += w;
         const float4 *src = reinterpret_cast<const float4 *>(
-            p.part_o + ((int64_t)(slot0 + s) * kTileRows + r) * kHeadDim + part * 32);
+            p.part_o + ((int64_t)(slot0 + s) * p.rows + r) * kHeadDim + part * 32);
 #pragma unroll
         for (int d = 0; d < 8; ++d) {
             const float4 v = src[d];
@@ -335,17 +336,22 @@ __global__ void __launch_bounds__(256) prefill_combine_kernel(const PrefillParam
     }
 }
 
+#include "prefill_tc.cuh"
+
+// query rows per tile of each kernel variant (0: tcgen05, 1: mma.sync)
+static int variant_rows(int variant) { return variant == 0 ? kTcRows : variant == 1 ? kTileRows : -1; }
+
 }  // namespace fs
 
 using namespace fs;
 
-extern "C" int fs_prefill_tokens_per_tile(int q_per_kv) {
-    if (q_per_kv < 1 || q_per_kv > FS_MAX_Q_PER_KV) return -1;
-    return kTileRows / q_per_kv;
+extern "C" int fs_prefill_tokens_per_tile(int q_per_kv, int variant) {
+    if (q_per_kv < 1 || q_per_kv > FS_MAX_Q_PER_KV || variant_rows(variant) < 0) return -1;
+    return variant_rows(variant) / q_per_kv;
 }
 
 extern "C" int fs_plan_prefill_tiles(int32_t n_items, const int32_t *item_start,
-                                     const int32_t *item_len, int32_t q_per_kv,
+                                     const int32_t *item_len, int32_t q_per_kv, int32_t variant,
                                      int32_t target_units, int32_t max_tiles, int32_t *tile_item,
                                      int32_t *tile_tok0, int32_t *tile_page0, int32_t *tile_page1,
                                      int32_t *tile_slot, int32_t *n_tiles, int32_t max_comb,
@@ -354,9 +360,10 @@ extern "C" int fs_plan_prefill_tiles(int32_t n_items, const int32_t *item_start,
     FS_CHECK_ARG(n_items >= 0, "n_items must be nonnegative");
     FS_CHECK_ARG(q_per_kv >= 1 && q_per_kv <= FS_MAX_Q_PER_KV, "q_per_kv must be in [1, %d]",
                  FS_MAX_Q_PER_KV);
+    FS_CHECK_ARG(variant_rows(variant) > 0, "unknown prefill kernel variant %d", variant);
     FS_CHECK_ARG(n_tiles && n_comb && n_slots, "null pointer");
     FS_CHECK_ARG(n_items == 0 || (item_start && item_len), "null item arrays");
-    const int tpt = kTileRows / q_per_kv;
+    const int tpt = variant_rows(variant) / q_per_kv;
     struct Tok { int32_t item, tok0, pages; };
     std::vector<Tok> toks;
     int64_t work = 0;
@@ -452,25 +459,36 @@ extern "C" int fs_prefill_attention(const fs_prefill_desc *d, void *stream) {
     prm.comb_slot0 = d->comb_slot0;
     prm.comb_nsplit = d->comb_nsplit;
     prm.qpk = d->q_per_kv;
-    prm.tpt = kTileRows / d->q_per_kv;
+    FS_CHECK_ARG(variant_rows(d->variant) > 0, "unknown prefill kernel variant %d", d->variant);
+    prm.rows = variant_rows(d->variant);
+    prm.tpt = prm.rows / d->q_per_kv;
     prm.scale_log2 = d->scale * 1.4426950408889634f;
     prm.part_o = d->part_o;
     prm.part_lse = d->part_lse;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    constexpr int S = kPrefillStages;
-    const size_t smem = (size_t)S * kPageBytes + 3 * S * 8;
-    static bool attr_set[64] = {false};
+    static bool attr_set[2][64] = {{false}};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (!attr_set[dev & 63]) {
-        FS_CUDA(cudaFuncSetAttribute(prefill_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-        attr_set[dev & 63] = true;
+    if (d->variant == 0) {
+        if (!attr_set[0][dev & 63]) {
+            FS_CUDA(cudaFuncSetAttribute(prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kTcSmem));
+            attr_set[0][dev & 63] = true;
+        }
+        prefill_tc_kernel<<<d->n_tiles, 192, kTcSmem, st>>>(prm);
+    } else {
+        constexpr int S = kPrefillStages;
+        const size_t smem = (size_t)S * kPageBytes + 3 * S * 8;
+        if (!attr_set[1][dev & 63]) {
+            FS_CUDA(cudaFuncSetAttribute(prefill_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+            attr_set[1][dev & 63] = true;
+        }
+        prefill_kernel<S><<<d->n_tiles, (kConsumerWarps + 2) * 32, smem, st>>>(prm);
     }
-    prefill_kernel<S><<<d->n_tiles, (kConsumerWarps + 2) * 32, smem, st>>>(prm);
     FS_CUDA(cudaGetLastError());
     if (d->n_comb > 0) {
-        prefill_combine_kernel<<<d->n_comb, 256, 0, st>>>(prm);
+        prefill_combine_kernel<<<d->n_comb, prm.rows * 4, 0, st>>>(prm);
         FS_CUDA(cudaGetLastError());
     }
     return FS_OK;

@@ -1,0 +1,376 @@
+// K8, tcgen05 variant: the chunked-prefill GQA tile on the 5th-generation
+// tensor cores with the accumulators in TMEM (included by prefill.cu inside
+// namespace fs).
+//
+// Tile = 128 query rows (128 / q_per_kv chunk tokens x q_per_kv heads) =
+// the UMMA M.  KV is consumed in blocks of 64 keys (4 pages).  Per block j:
+//     S_j[128 x 64]   = Q[128 x 128] . K_j^T     tcgen05.mma, bf16, -> TMEM
+//     P_j             = exp2(S_j*scale - m)       softmax warps, f16 -> smem
+//     O[128 x 128]   += P_j . V_j                 tcgen05.mma, f16, TMEM acc
+// Roles (192 threads): warps 0-3 = softmax / correction / epilogue (thread
+// = row = TMEM lane), warp 4 = TMA producer (each page = 4 bulk copies of
+// 2 KB atoms, so the K / V blocks land as UMMA-canonical SWIZZLE_128B tiles:
+// K as the K-major B of S, V as the MN-major B of P.V), warp 5 = MMA issuer
+// (one thread) + TMEM owner.  S is double-buffered in TMEM so S_{j+2} is
+// computed while the softmax warps work on S_{j+1}; P is double-buffered in
+// smem.  The running max is rescaled lazily (FA4): O and l are only
+// rescaled when a row's max grows by more than 2^8, so P <= 256 stays exact
+// in f16 and most blocks never touch O.
+//
+// TMEM: O at columns [0, 128), S buffers at [128, 192) and [192, 256).
+
+constexpr int kTcRows = 128;
+constexpr int kTcKeys = 64;                       // keys per block (4 pages)
+constexpr int kTcStages = 3;                      // K/V block ring
+constexpr int kTcQBytes = kTcRows * 256;          // 32 KB: 2 atoms x 128 rows x 128 B
+constexpr int kTcKVBytes = kTcKeys * 256;         // 16 KB: 2 atoms x 64 rows x 128 B
+constexpr int kTcPBytes = kTcRows * 128;          // 16 KB: 128 rows x 64 f16
+constexpr int kTcSmem = kTcQBytes + 2 * kTcStages * kTcKVBytes + 2 * kTcPBytes + 1024 + 256;
+constexpr float kTcRescale = 8.f;                 // lazy-rescale threshold (log2)
+
+// kind::f16 instruction descriptors: D fp32; S: A = Q bf16 K-major, B = K
+// bf16 K-major, M 128, N 64; PV: A = P f16 K-major, B = V f16 MN-major,
+// M 128, N 128
+constexpr uint32_t kIdescS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTcKeys >> 3) << 17) |
+                             ((uint32_t)(kTcRows >> 4) << 24);
+constexpr uint32_t kIdescPV = (1u << 4) | (1u << 16) | ((uint32_t)(kHeadDim >> 3) << 17) |
+                              ((uint32_t)(kTcRows >> 4) << 24);
+
+__device__ __forceinline__ uint64_t tc_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+    return d;
+}
+
+__device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_commit_bar(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     bar)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// 32 lanes x 32 consecutive fp32 columns (thread = lane = row)
+__device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+
+__device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+        "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+        "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+        "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void bulk_g2s_plain(uint32_t dst, const void *src, uint32_t bytes,
+                                               uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(192, 1) prefill_tc_kernel(const PrefillParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t sb = smem_u32(smem);
+    const uint32_t q_s = sb;
+    const uint32_t kv_s = q_s + kTcQBytes;                         // stage s: K at +2s*16K, V at +(2s+1)*16K
+    const uint32_t p_s = kv_s + 2 * kTcStages * kTcKVBytes;        // 2 P buffers
+    const uint32_t bars = p_s + 2 * kTcPBytes;
+    const uint32_t kv_full = bars, kv_empty = bars + 8 * kTcStages;
+    const uint32_t s_full = bars + 16 * kTcStages, s_free = s_full + 16;
+    const uint32_t p_full = s_free + 16, o_done = p_full + 16, q_ready = o_done + 16;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + (q_ready + 8 - sb));
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t = blockIdx.x;
+    const int item = p.tile_item[t];
+    const int tok0 = p.tile_tok0[t];
+    const int pg0 = p.tile_page0[t];
+    const int npg = p.tile_page1[t] - pg0;
+    const int nb = (npg + 3) >> 2;  // 64-key blocks
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTcStages; ++s) {
+            mbar_init(kv_full + 8 * s, 1);
+            mbar_init(kv_empty + 8 * s, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(s_full + 8 * b, 1);
+            mbar_init(s_free + 8 * b, 4);
+            mbar_init(p_full + 8 * b, 4);
+            mbar_init(o_done + 8 * b, 1);
+        }
+        mbar_init(q_ready, 4);
+        fence_barrier_init();
+    }
+    if (warp == 5) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                         smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_before();
+    __syncthreads();
+    tc_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 4) {
+        // ---------------- TMA producer ----------------
+        const int64_t row = (int64_t)p.item_seq[item] * p.bt_stride + pg0;
+        int64_t ids = 0;
+        for (int j = 0; j < nb; ++j) {
+            const int st = j % kTcStages;
+            if (j >= kTcStages) {
+                if (lane == 0) mbar_wait(kv_empty + 8 * st, ((j / kTcStages) - 1) & 1);
+                __syncwarp();
+            }
+            const int np = min(4, npg - 4 * j);
+            const uint32_t ks = kv_s + 2 * st * kTcKVBytes, vs = ks + kTcKVBytes;
+            if (np < 4) {
+                // keys of missing pages are masked; their V rows must be finite
+                const int per_atom = (4 - np) * 128;  // 16-byte chunks past page np-1
+                for (int c = lane; c < 2 * per_atom; c += 32) {
+                    const int a = c / per_atom, w = c - a * per_atom;
+                    reinterpret_cast<uint4 *>(smem + (vs - sb) + a * 8192 + np * 2048)[w] =
+                        make_uint4(0, 0, 0, 0);
+                }
+                fence_proxy_async();
+                __syncwarp();
+            }
+            for (int pp = 0; pp < np; ++pp) {
+                const int k = 4 * j + pp;
+                if ((k & 31) == 0) ids = k + lane < npg ? p.bt[row + k + lane] : 0;
+                const int64_t pg = __shfl_sync(0xffffffffu, ids, k & 31);
+                if (lane == 0) {
+                    if (pp == 0) mbar_expect_tx(kv_full + 8 * st, np * kPageBytes);
+                    const uint8_t *src = p.kv + pg * kPageBytes;
+                    for (int a = 0; a < 2; ++a) {
+                        bulk_g2s_plain(ks + a * 8192 + pp * 2048, src + a * kAtomBytes, kAtomBytes,
+                                       kv_full + 8 * st);
+                        bulk_g2s_plain(vs + a * 8192 + pp * 2048, src + kHalfPage + a * kAtomBytes,
+                                       kAtomBytes, kv_full + 8 * st);
+                    }
+                }
+            }
+        }
+    } else if (warp == 5) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            const uint32_t o_t = tmem, s_t = tmem + kHeadDim;
+            mbar_wait(q_ready, 0);
+            tc_after();
+            auto issue_s = [&](int j) {
+                const int st = j % kTcStages, b = j & 1;
+                if (j >= 2) mbar_wait(s_free + 8 * b, ((j >> 1) - 1) & 1);
+                mbar_wait(kv_full + 8 * st, (j / kTcStages) & 1);
+                tc_after();
+                const uint32_t ks = kv_s + 2 * st * kTcKVBytes;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint64_t ad = tc_desc(q_s + (k >> 2) * (kTcRows * 128) + (k & 3) * 32, 16, 1024);
+                    const uint64_t bd = tc_desc(ks + (k >> 2) * (kTcKeys * 128) + (k & 3) * 32, 16, 1024);
+                    tc_mma_f16(s_t + b * kTcKeys, ad, bd, kIdescS, k > 0);
+                }
+                tc_commit_bar(s_full + 8 * b);
+            };
+            issue_s(0);
+            if (nb > 1) issue_s(1);
+            for (int j = 0; j < nb; ++j) {
+                const int st = j % kTcStages, b = j & 1;
+                mbar_wait(p_full + 8 * b, (j >> 1) & 1);
+                tc_after();
+                const uint32_t vs = kv_s + (2 * st + 1) * kTcKVBytes;
+                const uint32_t ps = p_s + b * kTcPBytes;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint64_t ad = tc_desc(ps + k * 32, 16, 1024);
+                    const uint64_t bd = tc_desc(vs + k * 2048, kTcKeys * 128, 1024);
+                    tc_mma_f16(o_t, ad, bd, kIdescPV, (j > 0 || k > 0) ? 1u : 0u);
+                }
+                tc_commit_bar(kv_empty + 8 * st);
+                tc_commit_bar(o_done + 8 * b);
+                if (j + 2 < nb) issue_s(j + 2);
+            }
+        }
+    } else {
+        // ---------------- softmax / correction / epilogue (row = thread) ----------------
+        const int r = threadIdx.x;                       // 0..127
+        const int qpk = p.qpk, rows_used = p.tpt * qpk;
+        const int start = p.item_start[item], n = p.item_len[item];
+        const int tl = min(r, rows_used - 1) / qpk;
+        const int tok = min(tok0 + tl, n - 1);
+        const int h = r % qpk;
+        const bool valid = r < rows_used && tok0 + r / qpk < n;
+        const int pos = start + tok;                     // causal limit of this row
+        const int kv_lim = (pg0 + npg) * kPageTokens;    // keys past the range: masked
+        // ---- Q row -> smem (2 SW128 atoms) ----
+        {
+            const uint4 *src = reinterpret_cast<const uint4 *>(p.q + p.item_qoff[item] +
+                                                               (int64_t)tok * p.q_stride + h * kHeadDim);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                const uint4 v = src[c];
+                const uint32_t off = (c >> 3) * (kTcRows * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4);
+                *reinterpret_cast<uint4 *>(smem + (q_s - sb) + off) = v;
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cta(q_ready);
+        }
+        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+        const uint32_t o_t = tmem + lane_base, s_t = tmem + kHeadDim + lane_base;
+        float m_used = -INFINITY, l = 0.f;
+        for (int j = 0; j < nb; ++j) {
+            const int b = j & 1;
+            mbar_wait(s_full + 8 * b, (j >> 1) & 1);
+            tc_after();
+            uint32_t sr[2][32];
+            tc_ld32(s_t + b * kTcKeys, sr[0]);
+            tc_ld32(s_t + b * kTcKeys + 32, sr[1]);
+            tc_wait_ld();
+            tc_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cta(s_free + 8 * b);
+            const int kb0 = (pg0 + 4 * j) * kPageTokens;
+            float mx = -INFINITY;
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    const int key = kb0 + hh * 32 + c;
+                    float v = __uint_as_float(sr[hh][c]) * p.scale_log2;
+                    v = (key > pos || key >= kv_lim) ? -INFINITY : v;
+                    sr[hh][c] = __float_as_uint(v);
+                    mx = fmaxf(mx, v);
+                }
+            float alpha = 1.f;
+            const bool grow = mx > m_used + kTcRescale;
+            if (grow) {
+                alpha = m_used == -INFINITY ? 0.f : fast_exp2(m_used - mx);
+                m_used = mx;
+                l *= alpha;
+            }
+            if (j > 0 && __any_sync(0xffffffffu, grow)) {
+                // rescale this warp's O rows once P_{j-1} . V_{j-1} landed
+                mbar_wait(o_done + 8 * ((j - 1) & 1), ((j - 1) >> 1) & 1);
+                tc_after();
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) {
+                    uint32_t ov[32];
+                    tc_ld32(o_t + cc * 32, ov);
+                    tc_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * alpha);
+                    tc_st32(o_t + cc * 32, ov);
+                }
+                tc_wait_st();
+            }
+            const float mu = m_used == -INFINITY ? 0.f : m_used;
+            // P_j (f16) -> smem buffer b once P.V_{j-2} has consumed it
+            if (j >= 2) mbar_wait(o_done + 8 * b, ((j - 2) >> 1) & 1);
+            uint8_t *prow = smem + (p_s - sb) + b * kTcPBytes + r * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {  // 8 keys per 16-byte chunk
+                float e[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    e[i] = fast_exp2(__uint_as_float(sr[c >> 2][(c & 3) * 8 + i]) - mu);
+                    l += e[i];
+                }
+                uint4 pk;
+                pk.x = pack_f16(e[0], e[1]);
+                pk.y = pack_f16(e[2], e[3]);
+                pk.z = pack_f16(e[4], e[5]);
+                pk.w = pack_f16(e[6], e[7]);
+                *reinterpret_cast<uint4 *>(prow + ((c ^ (r & 7)) << 4)) = pk;
+            }
+            fence_proxy_async();
+            tc_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cta(p_full + 8 * b);
+        }
+        // ---- epilogue: O / l (or the split partial) ----
+        mbar_wait(o_done + 8 * ((nb - 1) & 1), ((nb - 1) >> 1) & 1);
+        tc_after();
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        const int slot = p.tile_slot[t];
+        const int64_t ob = p.item_ooff[item] + (int64_t)(tok0 + r / qpk) * p.o_stride + h * kHeadDim;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+            uint32_t ov[32];
+            tc_ld32(o_t + cc * 32, ov);
+            tc_wait_ld();
+            if (slot >= 0) {
+                float4 *dst = reinterpret_cast<float4 *>(
+                    p.part_o + ((int64_t)slot * kTcRows + r) * kHeadDim + cc * 32);
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    dst[c] = make_float4(__uint_as_float(ov[4 * c]) * inv, __uint_as_float(ov[4 * c + 1]) * inv,
+                                         __uint_as_float(ov[4 * c + 2]) * inv,
+                                         __uint_as_float(ov[4 * c + 3]) * inv);
+            } else if (valid) {
+                if (p.out_fp32) {
+                    float4 *dst = reinterpret_cast<float4 *>(static_cast<float *>(p.out) + ob + cc * 32);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        dst[c] = make_float4(__uint_as_float(ov[4 * c]) * inv,
+                                             __uint_as_float(ov[4 * c + 1]) * inv,
+                                             __uint_as_float(ov[4 * c + 2]) * inv,
+                                             __uint_as_float(ov[4 * c + 3]) * inv);
+                } else {
+                    uint4 *dst = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.out) + ob + cc * 32);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        uint4 pk;
+                        pk.x = pack_bf16(__uint_as_float(ov[8 * c]) * inv, __uint_as_float(ov[8 * c + 1]) * inv);
+                        pk.y = pack_bf16(__uint_as_float(ov[8 * c + 2]) * inv, __uint_as_float(ov[8 * c + 3]) * inv);
+                        pk.z = pack_bf16(__uint_as_float(ov[8 * c + 4]) * inv, __uint_as_float(ov[8 * c + 5]) * inv);
+                        pk.w = pack_bf16(__uint_as_float(ov[8 * c + 6]) * inv, __uint_as_float(ov[8 * c + 7]) * inv);
+                        dst[c] = pk;
+                    }
+                }
+            }
+        }
+        if (slot >= 0) p.part_lse[(int64_t)slot * kTcRows + r] = l > 0.f ? m_used + __log2f(l) : -INFINITY;
+    }
+    tc_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    }
+}

@@ -21,7 +21,10 @@ import torch
 from . import _native as N
 from .core import ValidationError
 
-_TILE_ROWS = 64
+# kernel variants: 0 = tcgen05 (TMEM accumulators, 128-row tiles), 1 =
+# mma.sync (64-row tiles)
+VARIANT_ROWS = {0: 128, 1: 64}
+DEFAULT_VARIANT = 0
 
 
 def _stream():
@@ -32,13 +35,16 @@ class PrefillTilePlan:
     """Host tile / split plan of one launch: depends only on the items'
     (start, length) lists, so layers with the same item structure share it."""
 
-    def __init__(self, starts, lens, q_per_kv: int, target_units: int):
+    def __init__(self, starts, lens, q_per_kv: int, target_units: int,
+                 variant: int = DEFAULT_VARIANT):
         starts = np.ascontiguousarray(np.asarray(starts, dtype=np.int32))
         lens = np.ascontiguousarray(np.asarray(lens, dtype=np.int32))
         n = starts.size
-        tpt = N.lib.fs_prefill_tokens_per_tile(q_per_kv)
+        tpt = N.lib.fs_prefill_tokens_per_tile(q_per_kv, variant)
         if tpt < 0:
-            raise ValidationError(f"q_per_kv must be in [1, {N.MAX_Q_PER_KV}]")
+            raise ValidationError(f"q_per_kv must be in [1, {N.MAX_Q_PER_KV}] and variant in "
+                                  f"{sorted(VARIANT_ROWS)}")
+        self.variant, self.rows = variant, VARIANT_ROWS[variant]
         # capacity bounds: one tile per token tile plus one per 32 pages of
         # its causal range (splits are >= 32 pages)
         n_tok = (lens.astype(np.int64) + tpt - 1) // tpt
@@ -52,7 +58,7 @@ class PrefillTilePlan:
         P = N.C.POINTER(I32)
         cast = (lambda a: a.ctypes.data_as(P))
         N.check(N.lib.fs_plan_prefill_tiles(
-            n, cast(starts), cast(lens), q_per_kv, int(target_units), max_tiles,
+            n, cast(starts), cast(lens), q_per_kv, variant, int(target_units), max_tiles,
             out["item"], out["tok0"], out["p0"], out["p1"], out["slot"], N.C.byref(nt),
             max_comb, comb["item"], comb["tok0"], comb["slot0"], comb["ns"], N.C.byref(nc),
             N.C.byref(ns)), "fs_plan_prefill_tiles")
@@ -84,7 +90,7 @@ class PrefillLaunch:
 
     def __init__(self, cache, item_seq, item_start, item_len, item_qoff, item_ooff,
                  target_units: int = None, tile_plan: PrefillTilePlan = None,
-                 upload: bool = True):
+                 upload: bool = True, variant: int = DEFAULT_VARIANT):
         arrs = [np.ascontiguousarray(np.asarray(a, dtype=np.int32))
                 for a in (item_seq, item_start, item_len, item_qoff, item_ooff)]
         n = arrs[0].size
@@ -99,7 +105,7 @@ class PrefillLaunch:
         if tile_plan is None:
             if target_units is None:
                 target_units = 4 * N.lib.fs_device_sms(cache.dev_index)
-            tile_plan = PrefillTilePlan(arrs[1], arrs[2], self.qpk, target_units)
+            tile_plan = PrefillTilePlan(arrs[1], arrs[2], self.qpk, target_units, variant)
         tp = tile_plan
         self.plan = tp
         self.n_items, self.n_tiles, self.n_comb, self.n_slots = n, tp.n_tiles, tp.n_comb, \
@@ -123,17 +129,18 @@ class PrefillLaunch:
             tab = torch.from_numpy(self.host_table).to(cache.device)
             po = pl = None
             if self.n_slots:
-                po = torch.empty((self.n_slots, _TILE_ROWS, N.HEAD_DIM), dtype=torch.float32,
+                po = torch.empty((self.n_slots, tp.rows, N.HEAD_DIM), dtype=torch.float32,
                                  device=cache.device)
-                pl = torch.empty((self.n_slots, _TILE_ROWS), dtype=torch.float32,
+                pl = torch.empty((self.n_slots, tp.rows), dtype=torch.float32,
                                  device=cache.device)
             self.bind(tab, 0, po, pl)
 
     def bind(self, table: torch.Tensor, base: int, part_o=None, part_lse=None) -> None:
         """Use ``table[base : base + len(host_table)]`` (int32, on the device)
-        and the given partial buffers (>= n_slots x 64 rows)."""
-        if self.n_slots and (part_o is None or part_o.shape[0] < self.n_slots):
-            raise ValidationError("split tiles need partial buffers of n_slots rows")
+        and the given partial buffers (>= n_slots slots of the variant's rows)."""
+        if self.n_slots and (part_o is None or
+                             part_o.numel() < self.n_slots * self.plan.rows * N.HEAD_DIM):
+            raise ValidationError("split tiles need partial buffers of n_slots slots")
         self._tab, self._base = table, base
         self.part_o, self.part_lse = part_o, part_lse
 
@@ -166,8 +173,9 @@ class PrefillLaunch:
             d.comb_item, d.comb_tok0 = self._p("c_item"), self._p("c_tok0")
             d.comb_slot0, d.comb_nsplit = self._p("c_slot0"), self._p("c_ns")
             d.part_o, d.part_lse = self.part_o.data_ptr(), self.part_lse.data_ptr()
-            d.partial_slots = self.part_o.shape[0]
+            d.partial_slots = self.part_o.numel() // (self.plan.rows * N.HEAD_DIM)
         d.n_comb = self.n_comb
         d.q_per_kv = self.qpk
+        d.variant = self.plan.variant
         d.scale = (1.0 / math.sqrt(N.HEAD_DIM)) if scale is None else float(scale)
         N.check(N.lib.fs_prefill_attention(N.C.byref(d), _stream()), "fs_prefill_attention")

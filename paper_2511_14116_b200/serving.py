@@ -150,8 +150,9 @@ class StepPlan:
             self._off[name] = o
             o += size
         slots = max([lp.n_slots for lp in self.prefill if lp is not None] + [0])
-        self.pf_part_o = torch.empty((max(1, slots), 64, hd), dtype=torch.float32, device=dev)
-        self.pf_part_lse = torch.empty((max(1, slots), 64), dtype=torch.float32, device=dev)
+        rows = max([lp.plan.rows for lp in self.prefill if lp is not None] + [64])
+        self.pf_part_o = torch.empty((max(1, slots), rows, hd), dtype=torch.float32, device=dev)
+        self.pf_part_lse = torch.empty((max(1, slots), rows), dtype=torch.float32, device=dev)
         o = pf_base
         for lp in self.prefill:
             if lp is not None:

@@ -94,9 +94,9 @@ def test_prefill_tile_planner():
     import ctypes as C
     from paper_2511_14116_b200 import _native as N
     rng = np.random.default_rng(0)
-    for qpk in (1, 3, 4, 8):
-        tpt = N.lib.fs_prefill_tokens_per_tile(qpk)
-        assert tpt == 64 // qpk
+    for qpk, variant in ((1, 0), (3, 1), (4, 0), (8, 1), (8, 0), (5, 0)):
+        tpt = N.lib.fs_prefill_tokens_per_tile(qpk, variant)
+        assert tpt == (128 if variant == 0 else 64) // qpk
         starts = rng.integers(0, 5000, size=12).astype(np.int32)
         lens = rng.integers(0, 300, size=12).astype(np.int32)
         for target in (1, 600, 100000):
@@ -105,7 +105,7 @@ def test_prefill_tile_planner():
             nt, nc, ns = C.c_int32(), C.c_int32(), C.c_int32()
             P = C.POINTER(C.c_int32)
             rc = N.lib.fs_plan_prefill_tiles(
-                12, starts.ctypes.data_as(P), lens.ctypes.data_as(P), qpk, target, cap,
+                12, starts.ctypes.data_as(P), lens.ctypes.data_as(P), qpk, variant, target, cap,
                 arr["i"], arr["t"], arr["a"], arr["b"], arr["s"], C.byref(nt), cap, arr["ci"],
                 arr["ct"], arr["c0"], arr["cn"], C.byref(nc), C.byref(ns))
             assert rc == 0
@@ -130,6 +130,6 @@ def test_prefill_tile_planner():
         # too small an output array is a ValidationError-class status
         one = (C.c_int32 * 1)()
         rc = N.lib.fs_plan_prefill_tiles(12, starts.ctypes.data_as(P), lens.ctypes.data_as(P),
-                                         qpk, 1, 1, one, one, one, one, one, C.byref(nt), 1,
+                                         qpk, variant, 1, 1, one, one, one, one, one, C.byref(nt), 1,
                                          one, one, one, one, C.byref(nc), C.byref(ns))
         assert rc == N.FS_EVALIDATION

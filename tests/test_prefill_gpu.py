@@ -34,7 +34,8 @@ def _cache(n_seq, capacity, qpk, seed=0):
     return PagedKVCache(work, capacity, qpk, device="cuda", page_order="shuffled", seed=seed)
 
 
-def _run_case(qpk, starts, lens, seed, target_units=None, q_pad=3, out_dtype=torch.float32):
+def _run_case(qpk, starts, lens, seed, target_units=None, q_pad=3, out_dtype=torch.float32,
+              variant=0):
     """Items = sequences; q / out rows strided like a fused projection row."""
     from oracle.attention import head_prefill
     from paper_2511_14116_b200.prefill import PrefillLaunch
@@ -61,7 +62,7 @@ def _run_case(qpk, starts, lens, seed, target_units=None, q_pad=3, out_dtype=tor
     row0 = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
     out = torch.full((T, stride), 7.0, dtype=out_dtype, device="cuda")
     launch = PrefillLaunch(cache, np.arange(n), starts, lens, row0 * stride, row0 * stride,
-                           target_units=target_units)
+                           target_units=target_units, variant=variant)
     launch(q.cuda(), stride, out, stride)
     torch.cuda.synchronize()
     got = out.float().cpu().numpy()
@@ -85,34 +86,42 @@ def _run_case(qpk, starts, lens, seed, target_units=None, q_pad=3, out_dtype=tor
     return launch
 
 
+VARIANTS = [0, 1]  # 0: tcgen05 / TMEM, 128-row tiles; 1: mma.sync, 64-row tiles
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("qpk", [1, 3, 4, 8])
-def test_prefill_ragged(qpk):
+def test_prefill_ragged(qpk, variant):
     """Ragged chunks: fresh prompts, continuation chunks at page and
     non-page boundaries, 1-token chunks, a long prefix, an empty item."""
     starts = [0, 0, 16, 37, 100, 1000, 5, 0]
     lens = [1, 70, 16, 9, 130, 40, 0, 17]
-    _run_case(qpk, starts, lens, seed=qpk)
+    _run_case(qpk, starts, lens, seed=qpk, variant=variant)
 
 
+@pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("qpk", [4, 8])
-def test_prefill_splits(qpk):
+def test_prefill_splits(qpk, variant):
     """Many KV splits per tile (forced by a large target) merge to the same
     result; split ranges cover every tile's causal range exactly once."""
     starts = [3000, 0, 700]
     lens = [33, 200, 64]
-    launch = _run_case(qpk, starts, lens, seed=10 + qpk, target_units=100000)
+    launch = _run_case(qpk, starts, lens, seed=10 + qpk, target_units=100000, variant=variant)
     assert launch.n_comb > 0 and launch.n_slots > launch.n_comb
 
 
-def test_prefill_single_long_chunk():
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_prefill_single_long_chunk(variant):
     """A 512-token continuation chunk behind a 4096-token prefix."""
-    _run_case(8, [4096], [512], seed=99)
+    _run_case(8, [4096], [512], seed=99, variant=variant)
 
 
-def test_prefill_bf16_output():
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_prefill_bf16_output(variant):
     """The bf16 output the mixed step feeds to the O projection."""
-    _run_case(4, [0, 300, 17], [100, 50, 1], seed=5, out_dtype=torch.bfloat16)
-    _run_case(8, [1000], [64], seed=6, target_units=100000, out_dtype=torch.bfloat16)
+    _run_case(4, [0, 300, 17], [100, 50, 1], seed=5, out_dtype=torch.bfloat16, variant=variant)
+    _run_case(8, [1000], [64], seed=6, target_units=100000, out_dtype=torch.bfloat16,
+              variant=variant)
 
 
 def test_prefill_reference_golden(golden):

@@ -9,6 +9,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--qpk", type=int, default=8)
 ap.add_argument("--cases", default="1x2048@0,1x2048@8192,8x256@4096,1x512@30000,64x32@2000")
 ap.add_argument("--iters", type=int, default=10)
+ap.add_argument("--variant", type=int, default=0)
 a = ap.parse_args()
 for case in a.cases.split(","):
     cnt, rest = case.split("x")
@@ -21,7 +22,8 @@ for case in a.cases.split(","):
     q = torch.randn((cnt * ln, stride), device="cuda").to(torch.bfloat16)
     out = torch.empty_like(q)
     row0 = np.arange(cnt) * ln * stride
-    L = PrefillLaunch(cache, np.arange(cnt), [st] * cnt, [ln] * cnt, row0, row0)
+    L = PrefillLaunch(cache, np.arange(cnt), [st] * cnt, [ln] * cnt, row0, row0,
+                      variant=a.variant)
     for _ in range(3):
         L(q, stride, out, stride)
     torch.cuda.synchronize()
@@ -31,5 +33,5 @@ for case in a.cases.split(","):
         L(q, stride, out, stride)
     e.record(); torch.cuda.synchronize()
     ms = s.elapsed_time(e) / a.iters
-    print(f"{case:16s} qpk {a.qpk}: {ms*1e3:8.1f} us  {L.flops/ms/1e9:7.1f} TFLOP/s  "
+    print(f"{case:16s} v{a.variant} qpk {a.qpk}: {ms*1e3:8.1f} us  {L.flops/ms/1e9:7.1f} TFLOP/s  "
           f"tiles {L.n_tiles} splits {L.n_comb}")
