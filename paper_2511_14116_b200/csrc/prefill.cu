@@ -282,13 +282,14 @@ __global__ void __launch_bounds__((kConsumerWarps + 2) * 32) prefill_kernel(cons
     }
 }
 
-// merge the page-range splits of one (item, token tile): 4 threads per row,
+// merge the page-range splits of one (item, token tile); grid.y = 64-row
+// slabs of the tile: 4 threads per row,
 // 32 dims each, log-sum-exp weights in base 2
-__global__ void __launch_bounds__(512) prefill_combine_kernel(const PrefillParams p) {
+__global__ void __launch_bounds__(256) prefill_combine_kernel(const PrefillParams p) {
     const int g = blockIdx.x;
     const int item = p.comb_item[g], tok0 = p.comb_tok0[g];
     const int slot0 = p.comb_slot0[g], ns = p.comb_nsplit[g];
-    const int r = threadIdx.x >> 2, part = threadIdx.x & 3;
+    const int r = blockIdx.y * 64 + (threadIdx.x >> 2), part = threadIdx.x & 3;  // 64-row slabs
     const int qpk = p.qpk, rows_used = p.tpt * qpk;
     if (r >= rows_used) return;
     const int tok = tok0 + r / qpk, h = r % qpk;
@@ -338,8 +339,11 @@ __global__ void __launch_bounds__(512) prefill_combine_kernel(const PrefillParam
 
 #include "prefill_tc.cuh"
 
-// query rows per tile of each kernel variant (0: tcgen05, 1: mma.sync)
-static int variant_rows(int variant) { return variant == 0 ? kTcRows : variant == 1 ? kTileRows : -1; }
+// query rows per tile of each kernel variant (0: tcgen05 with two 128-row
+// halves, 1: mma.sync, 2: tcgen05 with one 128-row half)
+static int variant_rows(int variant) {
+    return variant == 0 ? 2 * kTcRows : variant == 1 ? kTileRows : variant == 2 ? kTcRows : -1;
+}
 
 }  // namespace fs
 
@@ -466,16 +470,24 @@ extern "C" int fs_prefill_attention(const fs_prefill_desc *d, void *stream) {
     prm.part_o = d->part_o;
     prm.part_lse = d->part_lse;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    static bool attr_set[2][64] = {{false}};
+    static bool attr_set[3][64] = {{false}};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (d->variant == 0) {
-        if (!attr_set[0][dev & 63]) {
-            FS_CUDA(cudaFuncSetAttribute(prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kTcSmem));
-            attr_set[0][dev & 63] = true;
+    if (d->variant == 0 || d->variant == 2) {
+        const int v = d->variant == 0 ? 0 : 2;
+        if (!attr_set[v == 0 ? 0 : 2][dev & 63]) {
+            if (v == 0)
+                FS_CUDA(cudaFuncSetAttribute(prefill_tc_kernel<2>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem<2>()));
+            else
+                FS_CUDA(cudaFuncSetAttribute(prefill_tc_kernel<1>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem<1>()));
+            attr_set[v == 0 ? 0 : 2][dev & 63] = true;
         }
-        prefill_tc_kernel<<<d->n_tiles, 192, kTcSmem, st>>>(prm);
+        if (v == 0)
+            prefill_tc_kernel<2><<<d->n_tiles, 2 * 128 + 64, tc_smem<2>(), st>>>(prm);
+        else
+            prefill_tc_kernel<1><<<d->n_tiles, 128 + 64, tc_smem<1>(), st>>>(prm);
     } else {
         constexpr int S = kPrefillStages;
         const size_t smem = (size_t)S * kPageBytes + 3 * S * 8;
@@ -488,7 +500,7 @@ extern "C" int fs_prefill_attention(const fs_prefill_desc *d, void *stream) {
     }
     FS_CUDA(cudaGetLastError());
     if (d->n_comb > 0) {
-        prefill_combine_kernel<<<d->n_comb, prm.rows * 4, 0, st>>>(prm);
+        prefill_combine_kernel<<<dim3(d->n_comb, prm.rows / 64), 256, 0, st>>>(prm);
         FS_CUDA(cudaGetLastError());
     }
     return FS_OK;

@@ -2,13 +2,18 @@
 // tensor cores with the accumulators in TMEM (included by prefill.cu inside
 // namespace fs).
 //
-// Tile = 128 query rows (128 / q_per_kv chunk tokens x q_per_kv heads) =
-// the UMMA M.  KV is consumed in blocks of 64 keys (4 pages).  Per block j:
+// Tile = NQ x 128 query rows (NQ*128 / q_per_kv chunk tokens x q_per_kv
+// heads); each 128-row half is one UMMA M and has its own 4 softmax warps,
+// so with NQ = 2 the K/V blocks in smem feed two independent S / P / O
+// streams and the tensor pipe always has the other half's MMAs to run while
+// one half is in softmax (FA4's two-tile ping-pong).  KV is consumed in
+// blocks of 64 keys (4 pages).  Per block j and half h:
 //     S_j[128 x 64]   = Q[128 x 128] . K_j^T     tcgen05.mma, bf16, -> TMEM
 //     P_j             = exp2(S_j*scale - m)       softmax warps, f16 -> smem
 //     O[128 x 128]   += P_j . V_j                 tcgen05.mma, f16, TMEM acc
-// Roles (192 threads): warps 0-3 = softmax / correction / epilogue (thread
-// = row = TMEM lane), warp 4 = TMA producer (each page = 4 bulk copies of
+// Roles (NQ*128 + 64 threads): warps 0..4NQ-1 = softmax / correction /
+// epilogue (thread = row = TMEM lane; half h = warp / 4), warp 4NQ = TMA
+// producer (each page = 4 bulk copies of
 // 2 KB atoms, so the K / V blocks land as UMMA-canonical SWIZZLE_128B tiles:
 // K as the K-major B of S, V as the MN-major B of P.V), warp 5 = MMA issuer
 // (one thread) + TMEM owner.  S is double-buffered in TMEM so S_{j+2} is
@@ -17,15 +22,19 @@
 // rescaled when a row's max grows by more than 2^8, so P <= 256 stays exact
 // in f16 and most blocks never touch O.
 //
-// TMEM: O at columns [0, 128), S buffers at [128, 192) and [192, 256).
+// TMEM (half h at column 256h): O at [0, 128), S buffers at [128, 192) and
+// [192, 256).
 
-constexpr int kTcRows = 128;
+constexpr int kTcRows = 128;                      // rows per Q half-tile (UMMA M)
 constexpr int kTcKeys = 64;                       // keys per block (4 pages)
 constexpr int kTcStages = 3;                      // K/V block ring
 constexpr int kTcQBytes = kTcRows * 256;          // 32 KB: 2 atoms x 128 rows x 128 B
 constexpr int kTcKVBytes = kTcKeys * 256;         // 16 KB: 2 atoms x 64 rows x 128 B
 constexpr int kTcPBytes = kTcRows * 128;          // 16 KB: 128 rows x 64 f16
-constexpr int kTcSmem = kTcQBytes + 2 * kTcStages * kTcKVBytes + 2 * kTcPBytes + 1024 + 256;
+template <int NQ>
+constexpr int tc_smem() {
+    return NQ * kTcQBytes + 2 * kTcStages * kTcKVBytes + 2 * NQ * kTcPBytes + 1024 + 512;
+}
 constexpr float kTcRescale = 8.f;                 // lazy-rescale threshold (log2)
 
 // kind::f16 instruction descriptors: D fp32; S: A = Q bf16 K-major, B = K
@@ -102,18 +111,22 @@ __device__ __forceinline__ void bulk_g2s_plain(uint32_t dst, const void *src, ui
         : "memory");
 }
 
-__global__ void __launch_bounds__(192, 1) prefill_tc_kernel(const PrefillParams p) {
+template <int NQ>
+__global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const PrefillParams p) {
+    constexpr int kSoftWarps = 4 * NQ;
+    constexpr int kTmemCols = 256 * NQ;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sb = smem_u32(smem);
-    const uint32_t q_s = sb;
-    const uint32_t kv_s = q_s + kTcQBytes;                         // stage s: K at +2s*16K, V at +(2s+1)*16K
-    const uint32_t p_s = kv_s + 2 * kTcStages * kTcKVBytes;        // 2 P buffers
-    const uint32_t bars = p_s + 2 * kTcPBytes;
+    const uint32_t q_s = sb;                                       // half h at + h*32K
+    const uint32_t kv_s = q_s + NQ * kTcQBytes;                    // stage s: K at +2s*16K, V at +(2s+1)*16K
+    const uint32_t p_s = kv_s + 2 * kTcStages * kTcKVBytes;        // half h, buffer b at + (2h+b)*16K
+    const uint32_t bars = p_s + 2 * NQ * kTcPBytes;
     const uint32_t kv_full = bars, kv_empty = bars + 8 * kTcStages;
-    const uint32_t s_full = bars + 16 * kTcStages, s_free = s_full + 16;
-    const uint32_t p_full = s_free + 16, o_done = p_full + 16, q_ready = o_done + 16;
+    // per half h and buffer b: barrier + 8 * (2h + b)
+    const uint32_t s_full = bars + 16 * kTcStages, s_free = s_full + 16 * NQ;
+    const uint32_t p_full = s_free + 16 * NQ, o_done = p_full + 16 * NQ, q_ready = o_done + 16 * NQ;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + (q_ready + 8 - sb));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -129,18 +142,18 @@ __global__ void __launch_bounds__(192, 1) prefill_tc_kernel(const PrefillParams 
             mbar_init(kv_full + 8 * s, 1);
             mbar_init(kv_empty + 8 * s, 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < 2 * NQ; ++b) {
             mbar_init(s_full + 8 * b, 1);
             mbar_init(s_free + 8 * b, 4);
             mbar_init(p_full + 8 * b, 4);
             mbar_init(o_done + 8 * b, 1);
         }
-        mbar_init(q_ready, 4);
+        mbar_init(q_ready, kSoftWarps);
         fence_barrier_init();
     }
-    if (warp == 5) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
-                         smem_u32(tmem_slot)));
+    if (warp == kSoftWarps + 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)), "n"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_before();
@@ -148,7 +161,7 @@ __global__ void __launch_bounds__(192, 1) prefill_tc_kernel(const PrefillParams 
     tc_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 4) {
+    if (warp == kSoftWarps) {
         // ---------------- TMA producer ----------------
         const int64_t row = (int64_t)p.item_seq[item] * p.bt_stride + pg0;
         int64_t ids = 0;
@@ -187,76 +200,89 @@ __global__ void __launch_bounds__(192, 1) prefill_tc_kernel(const PrefillParams 
                 }
             }
         }
-    } else if (warp == 5) {
+    } else if (warp == kSoftWarps + 1) {
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
-            const uint32_t o_t = tmem, s_t = tmem + kHeadDim;
             mbar_wait(q_ready, 0);
             tc_after();
             auto issue_s = [&](int j) {
                 const int st = j % kTcStages, b = j & 1;
-                if (j >= 2) mbar_wait(s_free + 8 * b, ((j >> 1) - 1) & 1);
                 mbar_wait(kv_full + 8 * st, (j / kTcStages) & 1);
-                tc_after();
                 const uint32_t ks = kv_s + 2 * st * kTcKVBytes;
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const uint64_t ad = tc_desc(q_s + (k >> 2) * (kTcRows * 128) + (k & 3) * 32, 16, 1024);
-                    const uint64_t bd = tc_desc(ks + (k >> 2) * (kTcKeys * 128) + (k & 3) * 32, 16, 1024);
-                    tc_mma_f16(s_t + b * kTcKeys, ad, bd, kIdescS, k > 0);
+                for (int h = 0; h < NQ; ++h) {
+                    if (j >= 2) mbar_wait(s_free + 8 * (2 * h + b), ((j >> 1) - 1) & 1);
+                    tc_after();
+                    const uint32_t qh = q_s + h * kTcQBytes;
+                    const uint32_t s_t = tmem + 256 * h + kHeadDim + b * kTcKeys;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const uint64_t ad = tc_desc(qh + (k >> 2) * (kTcRows * 128) + (k & 3) * 32, 16, 1024);
+                        const uint64_t bd = tc_desc(ks + (k >> 2) * (kTcKeys * 128) + (k & 3) * 32, 16, 1024);
+                        tc_mma_f16(s_t, ad, bd, kIdescS, k > 0);
+                    }
+                    tc_commit_bar(s_full + 8 * (2 * h + b));
                 }
-                tc_commit_bar(s_full + 8 * b);
             };
             issue_s(0);
             if (nb > 1) issue_s(1);
             for (int j = 0; j < nb; ++j) {
                 const int st = j % kTcStages, b = j & 1;
-                mbar_wait(p_full + 8 * b, (j >> 1) & 1);
-                tc_after();
                 const uint32_t vs = kv_s + (2 * st + 1) * kTcKVBytes;
-                const uint32_t ps = p_s + b * kTcPBytes;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint64_t ad = tc_desc(ps + k * 32, 16, 1024);
-                    const uint64_t bd = tc_desc(vs + k * 2048, kTcKeys * 128, 1024);
-                    tc_mma_f16(o_t, ad, bd, kIdescPV, (j > 0 || k > 0) ? 1u : 0u);
+                for (int h = 0; h < NQ; ++h) {
+                    mbar_wait(p_full + 8 * (2 * h + b), (j >> 1) & 1);
+                    tc_after();
+                    const uint32_t ps = p_s + (2 * h + b) * kTcPBytes;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint64_t ad = tc_desc(ps + k * 32, 16, 1024);
+                        const uint64_t bd = tc_desc(vs + k * 2048, kTcKeys * 128, 1024);
+                        tc_mma_f16(tmem + 256 * h, ad, bd, kIdescPV, (j > 0 || k > 0) ? 1u : 0u);
+                    }
+                    tc_commit_bar(o_done + 8 * (2 * h + b));
                 }
                 tc_commit_bar(kv_empty + 8 * st);
-                tc_commit_bar(o_done + 8 * b);
                 if (j + 2 < nb) issue_s(j + 2);
             }
         }
     } else {
         // ---------------- softmax / correction / epilogue (row = thread) ----------------
-        const int r = threadIdx.x;                       // 0..127
+        const int h = warp >> 2;                          // Q half
+        const int r = threadIdx.x & 127;                  // row within the half = TMEM lane
+        const int R = h * kTcRows + r;                    // row within the tile
         const int qpk = p.qpk, rows_used = p.tpt * qpk;
         const int start = p.item_start[item], n = p.item_len[item];
-        const int tl = min(r, rows_used - 1) / qpk;
+        const int tl = min(R, rows_used - 1) / qpk;
         const int tok = min(tok0 + tl, n - 1);
-        const int h = r % qpk;
-        const bool valid = r < rows_used && tok0 + r / qpk < n;
+        const int hd = R % qpk;
+        const bool valid = R < rows_used && tok0 + R / qpk < n;
         const int pos = start + tok;                     // causal limit of this row
         const int kv_lim = (pg0 + npg) * kPageTokens;    // keys past the range: masked
-        // ---- Q row -> smem (2 SW128 atoms) ----
+        // smallest row position of this half (rows of a half are in token order)
+        const int pos_min = start + min(tok0 + min(h * kTcRows, rows_used - 1) / qpk, n - 1);
+        const float scale = p.scale_log2;
+        // ---- Q row -> smem (2 SW128 atoms of this half) ----
         {
             const uint4 *src = reinterpret_cast<const uint4 *>(p.q + p.item_qoff[item] +
-                                                               (int64_t)tok * p.q_stride + h * kHeadDim);
+                                                               (int64_t)tok * p.q_stride + hd * kHeadDim);
 #pragma unroll
             for (int c = 0; c < 16; ++c) {
                 const uint4 v = src[c];
-                const uint32_t off = (c >> 3) * (kTcRows * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4);
+                const uint32_t off = h * kTcQBytes + (c >> 3) * (kTcRows * 128) + r * 128 +
+                                     (((c & 7) ^ (r & 7)) << 4);
                 *reinterpret_cast<uint4 *>(smem + (q_s - sb) + off) = v;
             }
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) mbar_arrive_cta(q_ready);
         }
-        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-        const uint32_t o_t = tmem + lane_base, s_t = tmem + kHeadDim + lane_base;
+        const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+        const uint32_t o_t = tmem + 256 * h + lane_base, s_t = o_t + kHeadDim;
         float m_used = -INFINITY, l = 0.f;
         for (int j = 0; j < nb; ++j) {
-            const int b = j & 1;
-            mbar_wait(s_full + 8 * b, (j >> 1) & 1);
+            const int b = j & 1, hb = 2 * h + b;
+            mbar_wait(s_full + 8 * hb, (j >> 1) & 1);
             tc_after();
             uint32_t sr[2][32];
             tc_ld32(s_t + b * kTcKeys, sr[0]);
@@ -264,19 +290,29 @@ __global__ void __launch_bounds__(192, 1) prefill_tc_kernel(const PrefillParams 
             tc_wait_ld();
             tc_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_cta(s_free + 8 * b);
+            if (lane == 0) mbar_arrive_cta(s_free + 8 * hb);
             const int kb0 = (pg0 + 4 * j) * kPageTokens;
-            float mx = -INFINITY;
+            // raw scores: the scale is folded into the exponent's FFMA; the
+            // mask only runs on blocks crossing a row's diagonal or the range
+            // end (warp-uniform test on the half's smallest row position)
+            if (kb0 + kTcKeys - 1 > pos_min || kb0 + kTcKeys > kv_lim) {
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) {
+                        const int key = kb0 + hh * 32 + c;
+                        if (key > pos || key >= kv_lim) sr[hh][c] = __float_as_uint(-INFINITY);
+                    }
+            }
+            float mxs[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) mxs[i] = -INFINITY;
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh)
 #pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    const int key = kb0 + hh * 32 + c;
-                    float v = __uint_as_float(sr[hh][c]) * p.scale_log2;
-                    v = (key > pos || key >= kv_lim) ? -INFINITY : v;
-                    sr[hh][c] = __float_as_uint(v);
-                    mx = fmaxf(mx, v);
-                }
+                for (int c = 0; c < 32; ++c) mxs[c & 7] = fmaxf(mxs[c & 7], __uint_as_float(sr[hh][c]));
+            const float mx = fmaxf(fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3])),
+                                   fmaxf(fmaxf(mxs[4], mxs[5]), fmaxf(mxs[6], mxs[7]))) * scale;
             float alpha = 1.f;
             const bool grow = mx > m_used + kTcRescale;
             if (grow) {
@@ -286,7 +322,7 @@ __global__ void __launch_bounds__(192, 1) prefill_tc_kernel(const PrefillParams 
             }
             if (j > 0 && __any_sync(0xffffffffu, grow)) {
                 // rescale this warp's O rows once P_{j-1} . V_{j-1} landed
-                mbar_wait(o_done + 8 * ((j - 1) & 1), ((j - 1) >> 1) & 1);
+                mbar_wait(o_done + 8 * (2 * h + ((j - 1) & 1)), ((j - 1) >> 1) & 1);
                 tc_after();
 #pragma unroll
                 for (int cc = 0; cc < 4; ++cc) {
@@ -300,16 +336,17 @@ __global__ void __launch_bounds__(192, 1) prefill_tc_kernel(const PrefillParams 
                 tc_wait_st();
             }
             const float mu = m_used == -INFINITY ? 0.f : m_used;
+            float ls[4] = {0.f, 0.f, 0.f, 0.f};
             // P_j (f16) -> smem buffer b once P.V_{j-2} has consumed it
-            if (j >= 2) mbar_wait(o_done + 8 * b, ((j - 2) >> 1) & 1);
-            uint8_t *prow = smem + (p_s - sb) + b * kTcPBytes + r * 128;
+            if (j >= 2) mbar_wait(o_done + 8 * hb, ((j - 2) >> 1) & 1);
+            uint8_t *prow = smem + (p_s - sb) + hb * kTcPBytes + r * 128;
 #pragma unroll
             for (int c = 0; c < 8; ++c) {  // 8 keys per 16-byte chunk
                 float e[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                    e[i] = fast_exp2(__uint_as_float(sr[c >> 2][(c & 3) * 8 + i]) - mu);
-                    l += e[i];
+                    e[i] = fast_exp2(fmaf(__uint_as_float(sr[c >> 2][(c & 3) * 8 + i]), scale, -mu));
+                    ls[i & 3] += e[i];
                 }
                 uint4 pk;
                 pk.x = pack_f16(e[0], e[1]);
@@ -318,17 +355,19 @@ __global__ void __launch_bounds__(192, 1) prefill_tc_kernel(const PrefillParams 
                 pk.w = pack_f16(e[6], e[7]);
                 *reinterpret_cast<uint4 *>(prow + ((c ^ (r & 7)) << 4)) = pk;
             }
+            l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
             fence_proxy_async();
             tc_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_cta(p_full + 8 * b);
+            if (lane == 0) mbar_arrive_cta(p_full + 8 * hb);
         }
         // ---- epilogue: O / l (or the split partial) ----
-        mbar_wait(o_done + 8 * ((nb - 1) & 1), ((nb - 1) >> 1) & 1);
+        mbar_wait(o_done + 8 * (2 * h + ((nb - 1) & 1)), ((nb - 1) >> 1) & 1);
         tc_after();
         const float inv = l > 0.f ? 1.f / l : 0.f;
         const int slot = p.tile_slot[t];
-        const int64_t ob = p.item_ooff[item] + (int64_t)(tok0 + r / qpk) * p.o_stride + h * kHeadDim;
+        const int rows = p.rows;
+        const int64_t ob = p.item_ooff[item] + (int64_t)(tok0 + R / qpk) * p.o_stride + hd * kHeadDim;
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) {
             uint32_t ov[32];
@@ -336,7 +375,7 @@ __global__ void __launch_bounds__(192, 1) prefill_tc_kernel(const PrefillParams 
             tc_wait_ld();
             if (slot >= 0) {
                 float4 *dst = reinterpret_cast<float4 *>(
-                    p.part_o + ((int64_t)slot * kTcRows + r) * kHeadDim + cc * 32);
+                    p.part_o + ((int64_t)slot * rows + R) * kHeadDim + cc * 32);
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
                     dst[c] = make_float4(__uint_as_float(ov[4 * c]) * inv, __uint_as_float(ov[4 * c + 1]) * inv,
@@ -365,12 +404,12 @@ __global__ void __launch_bounds__(192, 1) prefill_tc_kernel(const PrefillParams 
                 }
             }
         }
-        if (slot >= 0) p.part_lse[(int64_t)slot * kTcRows + r] = l > 0.f ? m_used + __log2f(l) : -INFINITY;
+        if (slot >= 0) p.part_lse[(int64_t)slot * rows + R] = l > 0.f ? m_used + __log2f(l) : -INFINITY;
     }
     tc_before();
     __syncthreads();
-    if (warp == 5) {
+    if (warp == kSoftWarps + 1) {
         tc_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
     }
 }

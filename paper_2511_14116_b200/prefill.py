@@ -21,9 +21,9 @@ import torch
 from . import _native as N
 from .core import ValidationError
 
-# kernel variants: 0 = tcgen05 (TMEM accumulators, 128-row tiles), 1 =
-# mma.sync (64-row tiles)
-VARIANT_ROWS = {0: 128, 1: 64}
+# kernel variants: 0 = tcgen05 (TMEM accumulators, two 128-row halves per
+# tile), 1 = mma.sync (64-row tiles), 2 = tcgen05 with one 128-row half
+VARIANT_ROWS = {0: 256, 1: 64, 2: 128}
 DEFAULT_VARIANT = 0
 
 

@@ -94,9 +94,9 @@ def test_prefill_tile_planner():
     import ctypes as C
     from paper_2511_14116_b200 import _native as N
     rng = np.random.default_rng(0)
-    for qpk, variant in ((1, 0), (3, 1), (4, 0), (8, 1), (8, 0), (5, 0)):
+    for qpk, variant in ((1, 0), (3, 1), (4, 0), (8, 1), (8, 0), (5, 0), (3, 2)):
         tpt = N.lib.fs_prefill_tokens_per_tile(qpk, variant)
-        assert tpt == (128 if variant == 0 else 64) // qpk
+        assert tpt == {0: 256, 1: 64, 2: 128}[variant] // qpk
         starts = rng.integers(0, 5000, size=12).astype(np.int32)
         lens = rng.integers(0, 300, size=12).astype(np.int32)
         for target in (1, 600, 100000):

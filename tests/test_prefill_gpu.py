@@ -86,7 +86,8 @@ def _run_case(qpk, starts, lens, seed, target_units=None, q_pad=3, out_dtype=tor
     return launch
 
 
-VARIANTS = [0, 1]  # 0: tcgen05 / TMEM, 128-row tiles; 1: mma.sync, 64-row tiles
+# 0: tcgen05 / TMEM, 2 x 128-row halves; 1: mma.sync, 64-row tiles; 2: tcgen05, 128 rows
+VARIANTS = [0, 1, 2]
 
 
 @pytest.mark.parametrize("variant", VARIANTS)

@@ -10,6 +10,7 @@ ap.add_argument("--qpk", type=int, default=8)
 ap.add_argument("--cases", default="1x2048@0,1x2048@8192,8x256@4096,1x512@30000,64x32@2000")
 ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--variant", type=int, default=0)
+ap.add_argument("--target", type=int, default=None, help="target_units of the tile planner")
 a = ap.parse_args()
 for case in a.cases.split(","):
     cnt, rest = case.split("x")
@@ -23,7 +24,7 @@ for case in a.cases.split(","):
     out = torch.empty_like(q)
     row0 = np.arange(cnt) * ln * stride
     L = PrefillLaunch(cache, np.arange(cnt), [st] * cnt, [ln] * cnt, row0, row0,
-                      variant=a.variant)
+                      variant=a.variant, target_units=a.target)
     for _ in range(3):
         L(q, stride, out, stride)
     torch.cuda.synchronize()
