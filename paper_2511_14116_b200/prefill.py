@@ -27,6 +27,12 @@ VARIANT_ROWS = {0: 256, 1: 64, 2: 128}
 DEFAULT_VARIANT = 0
 
 
+def default_target_units(device_index: int, variant: int = DEFAULT_VARIANT) -> int:
+    """Tiles the planner aims for: 2 per SM for the tcgen05 variants (one
+    ~225-KB CTA per SM), 4 per SM for the mma.sync variant."""
+    return (4 if variant == 1 else 2) * N.lib.fs_device_sms(device_index)
+
+
 def _stream():
     return N.C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
@@ -104,7 +110,7 @@ class PrefillLaunch:
         self.qpk = cache.qpk
         if tile_plan is None:
             if target_units is None:
-                target_units = 4 * N.lib.fs_device_sms(cache.dev_index)
+                target_units = default_target_units(cache.dev_index, variant)
             tile_plan = PrefillTilePlan(arrs[1], arrs[2], self.qpk, target_units, variant)
         tp = tile_plan
         self.plan = tp

@@ -36,7 +36,7 @@ import torch
 from . import _native as N
 from .core import ValidationError
 from .hybrid import HybridDecodeRank
-from .prefill import PrefillLaunch, PrefillTilePlan
+from .prefill import PrefillLaunch, PrefillTilePlan, default_target_units
 
 
 @dataclass
@@ -85,7 +85,7 @@ class StepPlan:
         dec_seg = [0]
         self.prefill = []
         tile_plans = {}
-        target = 4 * N.lib.fs_device_sms(eng.cache.dev_index)
+        target = default_target_units(eng.cache.dev_index)
         n_kv = n_dec = 0
         for layer in range(L):
             idx = eng.item_index[layer]

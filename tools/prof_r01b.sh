@@ -9,6 +9,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/launches.csv $BENCH > $OUT/launches_bench.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:decode \
     -s 40 -c 1 -o $OUT/decode_full $BENCH > $OUT/full_bench.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:prefill_kernel \
-    -s 2 -c 1 -o $OUT/prefill_full python tools/prefill_bench.py --cases 1x2048@8192 --iters 2 > $OUT/full_prefill.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:prefill_tc \
+    -s 3 -c 1 -o $OUT/prefill_full python tools/prefill_bench.py --cases 1x2048@8192 --iters 2 > $OUT/full_prefill.log 2>&1
 ls -la $OUT
