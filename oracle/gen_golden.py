@@ -240,6 +240,29 @@ def gen_prefill():
     return {"head_dim": hd, "cases": cases}
 
 
+def gen_metrics():
+    """A small live-reference simulation (Llama-70B config, bundled
+    mooncake_small trace head, one GPU failure): its JSONL records and
+    report.summarize() of them -- the wire format the B200 runs emit."""
+    import tempfile
+    from failsafe.recovery import load_failure_trace
+    from failsafe.report import summarize
+    from failsafe.simulation import MetricsLog, run_simulation
+    from failsafe.traces import load_request_trace
+    model, cluster = load_config(os.path.join(DATA, "llama70b.toml"))
+    with open(os.path.join(DATA, "traces", "mooncake_small.csv")) as fh:
+        rows = load_request_trace(fh.read())[:24]
+    fails = load_failure_trace("ts_s,event,gpu_id\n6.0,fail,7\n")
+    log = run_simulation(model, cluster, "hybrid", "load_aware", rows, fails,
+                         record_iterations=True, max_time=60.0)
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "m.jsonl")
+        log.write_jsonl(path)
+        text = open(path).read()
+        summ = summarize(MetricsLog.read_jsonl(path))
+    return {"jsonl": text, "summary": summ}
+
+
 def toy_model(L, H, shards, qpk=1):
     return ModelSpec(num_layers=L, num_kv_heads=H, num_q_heads=H * qpk, head_dim=8,
                      hidden_dim=32, ffn_intermediate_dim=96, ffn_num_shards=shards)
@@ -411,7 +434,7 @@ def main():
     os.makedirs(OUT, exist_ok=True)
     gens = (("placement", gen_placement), ("routing", gen_routing),
             ("recovery", gen_recovery), ("forward", gen_forward), ("decode", gen_decode),
-            ("batches", gen_batches), ("prefill", gen_prefill))
+            ("batches", gen_batches), ("prefill", gen_prefill), ("metrics", gen_metrics))
     only = sys.argv[1:]
     for name, fn in gens:
         if only and name not in only:

@@ -40,6 +40,7 @@ import torch
 
 from . import _native as N
 from .core import Request, ValidationError
+from .metrics import MetricsLog, RunRecorder
 from .placement import make_placement, owner_array
 from .recovery import BackupState, plan_kv_recovery, plan_weight_recovery
 from .recovery_exec import KVBackupExecutor, restore_pages
@@ -102,7 +103,7 @@ class EmulatedCluster:
         self.alive = list(range(world))
         self.plan = make_placement("hybrid", model, self.alive)
         self.budget = token_budget
-        self.requests = [Request(id=i, arrival_time=float(i), input_len=a, output_len=o)
+        self.requests = [Request(id=i, arrival_time=0.0, input_len=a, output_len=o)
                          for i, (a, o) in enumerate(inputs)]
         self.caps = np.array([a + o - 1 for a, o in inputs], dtype=np.int64)
         self.max_tokens = token_budget + len(inputs)
@@ -112,6 +113,11 @@ class EmulatedCluster:
         self.token_x = {}  # (request, position) -> the token's input row (host), for recompute
         self.engines = self._build(self.plan, self.routing, self.alive)
         self.backups = {g: KVBackupExecutor(e.cache) for g, e in self.engines.items()}
+        # reference-format metrics (simulation.py:84-132) on the measured
+        # clock: every rank of the world shares this GPU, so an iteration's
+        # duration is the sum of the ranks' work (a real world runs them in
+        # parallel)
+        self.recorder = RunRecorder(self.requests, world)
 
     def _build(self, plan, routing, ranks):
         owner = owner_array(plan, self.model.num_kv_heads)
@@ -138,7 +144,12 @@ class EmulatedCluster:
         the tokens' inputs, advance request progress and back up every page
         that became complete (K5 on each rank's side stream)."""
         ranks = [self.engines[g] for g in self.alive]
-        out = emulated_serving_step(ranks, [e.plan(batch) for e in ranks], x.to(self.device))
+        plans = [e.plan(batch) for e in ranks]
+        x = x.to(self.device)
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        out = emulated_serving_step(ranks, plans, x)
+        t1.record()
         xh = x.detach().to("cpu")
         rows = [(r, s + j) for r, s, n in batch.prefill for j in range(n)] + list(batch.decode)
         for t, key in enumerate(rows):
@@ -149,13 +160,22 @@ class EmulatedCluster:
             req = self.requests[rid]
             req.tokens_decoded += 1
             self.sched.note_decode_token(req, self.routing[rid])
+        first = []
         for req in self.requests:
             if req.tokens_prefilled == req.input_len and req.tokens_decoded == 0:
                 req.tokens_decoded = 1
+                first.append(req.id)
         marks = {r.id: self.context(r.id) for r in self.requests}
         for ex in self.backups.values():
             ex.sync(marks)
+        t1.synchronize()
+        self.recorder.iteration(batch, t0.elapsed_time(t1) / 1e3, finished_prefill=first)
         return out
+
+    def metrics(self) -> MetricsLog:
+        """The run so far as the reference's JSONL records (+ run_summary)."""
+        unserved = sum(1 for r in self.requests if r.tokens_decoded < r.output_len)
+        return self.recorder.finish(unserved)
 
     # ----------------------------------------------------------- failover --
     def fail(self, gpu: int) -> FailoverReport:
@@ -259,6 +279,9 @@ class EmulatedCluster:
         marks = {r.id: self.context(r.id) for r in self.requests}
         for ex in self.backups.values():
             ex.sync(marks)
+        self.recorder.failure(gpu, alive=len(survivors))
+        self.recorder.reconfig(len(survivors), rep.recovery_ms / 1e3, rep.recompute_tokens,
+                               rep.kv_restore_bytes + rep.weight_h2d_bytes)
         return rep
 
 

@@ -55,3 +55,14 @@ def test_failover_resumes_with_identical_outputs(world, fails):
     # every request finishes on the shrunk world
     run(40)
     assert all(r.tokens_decoded == r.output_len for r in cl.requests)
+    # the measured run in the reference's metrics wire format
+    from paper_2511_14116_b200.metrics import summarize
+    log = cl.metrics()
+    kinds = [r["kind"] for r in log.records]
+    assert kinds.count("request") == len(inputs) and kinds.count("failure") == len(fails)
+    assert kinds.count("reconfig_done") == len(fails) and kinds[-1] == "run_summary"
+    s = summarize(log)
+    assert s["requests_completed"] == len(inputs)
+    assert s["prefill_tokens"] == sum(a for a, _ in inputs)
+    assert s["decode_tokens"] == sum(o for _, o in inputs)
+    assert s["ttft"]["max"] > 0 and s["tbt"]["max"] > 0
