@@ -381,9 +381,17 @@ extern "C" int fs_plan_prefill_tiles(int32_t n_items, const int32_t *item_start,
         }
     }
     // pages per split: at least 32 (a split below that is all pipeline
-    // fill), at most what gives ~target_units equal tiles
+    // fill); grown until the tile count fits in target_units, so a launch of
+    // similar tiles is whole waves (a partial last wave of equal-size tiles
+    // idles the other SMs for a full tile time)
     const int64_t units = std::max<int64_t>(1, target_units);
-    const int32_t per = (int32_t)std::max<int64_t>(32, (work + units - 1) / units);
+    int32_t per = (int32_t)std::max<int64_t>(32, (work + units - 1) / units);
+    auto count = [&](int32_t q) {
+        int64_t n = 0;
+        for (const Tok &tk : toks) n += (tk.pages + q - 1) / q;
+        return n;
+    };
+    while ((int64_t)toks.size() < units && count(per) > units) per += std::max(1, per / 16);
     struct Tile { int32_t item, tok0, p0, p1, slot; };
     std::vector<Tile> tiles;
     int32_t slots = 0, nc = 0;
