@@ -404,15 +404,16 @@ def test_engine_graph_capture_replays_identically():
     e = _engines(model, "hybrid", 1, lens, {0: 0, 1: 0, 2: 0}, 1, kv_hist, mlp=True)[0]
     eager = e.step(x0.cuda()).clone()
     e.capture()
-    graphed = e.step(x0.cuda()).clone()
-    assert torch.equal(eager, graphed)
+    for _ in range(3):
+        graphed = e.step(x0.cuda()).clone()
+        assert torch.equal(eager, graphed)
 
 
 @pytest.mark.parametrize("qpk", [4, 8])
 def test_decode_long_context_per_item_tolerance(qpk):
     """The tolerance holds per long item, not only diluted over a launch:
-    bf16 P alone gives ~1.5e-3 mean-rel at 4k context; the kernels carry P
-    as a bf16 hi/lo pair."""
+    bf16 P alone gives ~1.5e-3 mean-rel at 4k context; the kernels use f16
+    P against the f16 V pages."""
     from oracle.attention import head_decode
     from oracle.placement import owner_table
     owner = owner_table("hybrid", 1, 8, range(8))
