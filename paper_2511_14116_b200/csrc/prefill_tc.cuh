@@ -9,7 +9,7 @@
 // one half is in softmax (FA4's two-tile ping-pong).  KV is consumed in
 // blocks of 64 keys (4 pages).  Per block j and half h:
 //     S_j[128 x 64]   = Q[128 x 128] . K_j^T     tcgen05.mma, bf16, -> TMEM
-//     P_j             = exp2(S_j*scale - m)       softmax warps, f16 -> smem
+//     P_j             = exp2(S_j*scale - m)       softmax warps, f16 -> TMEM
 //     O[128 x 128]   += P_j . V_j                 tcgen05.mma, f16, TMEM acc
 // Roles (NQ*128 + 64 threads): warps 0..4NQ-1 = softmax / correction /
 // epilogue (thread = row = TMEM lane; half h = warp / 4), warp 4NQ = TMA
@@ -17,8 +17,9 @@
 // 2 KB atoms, so the K / V blocks land as UMMA-canonical SWIZZLE_128B tiles:
 // K as the K-major B of S, V as the MN-major B of P.V), warp 5 = MMA issuer
 // (one thread) + TMEM owner.  S is double-buffered in TMEM so S_{j+2} is
-// computed while the softmax warps work on S_{j+1}; P is double-buffered in
-// smem.  The running max is rescaled lazily (FA4): O and l are only
+// computed while the softmax warps work on S_{j+1}; the softmax warps store
+// P (f16) over S_j's columns and P.V_j reads its A operand from TMEM (no
+// shared-memory round trip).  The running max is rescaled lazily (FA4): O and l are only
 // rescaled when a row's max grows by more than 2^8, so P <= 256 stays exact
 // in f16 and most blocks never touch O.
 //
@@ -27,13 +28,12 @@
 
 constexpr int kTcRows = 128;                      // rows per Q half-tile (UMMA M)
 constexpr int kTcKeys = 64;                       // keys per block (4 pages)
-constexpr int kTcStages = 3;                      // K/V block ring
+constexpr int kTcStages = 5;                      // K/V block ring
 constexpr int kTcQBytes = kTcRows * 256;          // 32 KB: 2 atoms x 128 rows x 128 B
 constexpr int kTcKVBytes = kTcKeys * 256;         // 16 KB: 2 atoms x 64 rows x 128 B
-constexpr int kTcPBytes = kTcRows * 128;          // 16 KB: 128 rows x 64 f16
 template <int NQ>
 constexpr int tc_smem() {
-    return NQ * kTcQBytes + 2 * kTcStages * kTcKVBytes + 2 * NQ * kTcPBytes + 1024 + 512;
+    return NQ * kTcQBytes + 2 * kTcStages * kTcKVBytes + 1024 + 512;
 }
 constexpr float kTcRescale = 8.f;                 // lazy-rescale threshold (log2)
 
@@ -62,6 +62,18 @@ __device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint64_t a_desc, uin
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// D[tmem] (+)= A[tmem] . B[smem]: A (K-major, 2 f16 per 32-bit column) read
+// straight from TMEM -- the softmax warps store P over their S columns
+__device__ __forceinline__ void tc_mma_f16_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                              uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
 
@@ -121,12 +133,11 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
     const uint32_t sb = smem_u32(smem);
     const uint32_t q_s = sb;                                       // half h at + h*32K
     const uint32_t kv_s = q_s + NQ * kTcQBytes;                    // stage s: K at +2s*16K, V at +(2s+1)*16K
-    const uint32_t p_s = kv_s + 2 * kTcStages * kTcKVBytes;        // half h, buffer b at + (2h+b)*16K
-    const uint32_t bars = p_s + 2 * NQ * kTcPBytes;
+    const uint32_t bars = kv_s + 2 * kTcStages * kTcKVBytes;
     const uint32_t kv_full = bars, kv_empty = bars + 8 * kTcStages;
     // per half h and buffer b: barrier + 8 * (2h + b)
-    const uint32_t s_full = bars + 16 * kTcStages, s_free = s_full + 16 * NQ;
-    const uint32_t p_full = s_free + 16 * NQ, o_done = p_full + 16 * NQ, q_ready = o_done + 16 * NQ;
+    const uint32_t s_full = bars + 16 * kTcStages;
+    const uint32_t p_full = s_full + 16 * NQ, o_done = p_full + 16 * NQ, q_ready = o_done + 16 * NQ;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + (q_ready + 8 - sb));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -144,7 +155,6 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
         }
         for (int b = 0; b < 2 * NQ; ++b) {
             mbar_init(s_full + 8 * b, 1);
-            mbar_init(s_free + 8 * b, 4);
             mbar_init(p_full + 8 * b, 4);
             mbar_init(o_done + 8 * b, 1);
         }
@@ -211,7 +221,9 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
                 const uint32_t ks = kv_s + 2 * st * kTcKVBytes;
 #pragma unroll
                 for (int h = 0; h < NQ; ++h) {
-                    if (j >= 2) mbar_wait(s_free + 8 * (2 * h + b), ((j >> 1) - 1) & 1);
+                    // S_j overwrites the TMEM columns P_{j-2} occupied: the
+                    // tensor pipe runs this thread's MMAs in issue order, so
+                    // P.V_{j-2} (issued earlier) has read them
                     tc_after();
                     const uint32_t qh = q_s + h * kTcQBytes;
                     const uint32_t s_t = tmem + 256 * h + kHeadDim + b * kTcKeys;
@@ -233,12 +245,11 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
                 for (int h = 0; h < NQ; ++h) {
                     mbar_wait(p_full + 8 * (2 * h + b), (j >> 1) & 1);
                     tc_after();
-                    const uint32_t ps = p_s + (2 * h + b) * kTcPBytes;
+                    const uint32_t pt = tmem + 256 * h + kHeadDim + b * kTcKeys;  // P over S_j
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
-                        const uint64_t ad = tc_desc(ps + k * 32, 16, 1024);
                         const uint64_t bd = tc_desc(vs + k * 2048, kTcKeys * 128, 1024);
-                        tc_mma_f16(tmem + 256 * h, ad, bd, kIdescPV, (j > 0 || k > 0) ? 1u : 0u);
+                        tc_mma_f16_ta(tmem + 256 * h, pt + k * 8, bd, kIdescPV, (j > 0 || k > 0) ? 1u : 0u);
                     }
                     tc_commit_bar(o_done + 8 * (2 * h + b));
                 }
@@ -288,9 +299,6 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
             tc_ld32(s_t + b * kTcKeys, sr[0]);
             tc_ld32(s_t + b * kTcKeys + 32, sr[1]);
             tc_wait_ld();
-            tc_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cta(s_free + 8 * hb);
             const int kb0 = (pg0 + 4 * j) * kPageTokens;
             // raw scores: the scale is folded into the exponent's FFMA; the
             // mask only runs on blocks crossing a row's diagonal or the range
@@ -337,26 +345,19 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
             }
             const float mu = m_used == -INFINITY ? 0.f : m_used;
             float ls[4] = {0.f, 0.f, 0.f, 0.f};
-            // P_j (f16) -> smem buffer b once P.V_{j-2} has consumed it
-            if (j >= 2) mbar_wait(o_done + 8 * hb, ((j - 2) >> 1) & 1);
-            uint8_t *prow = smem + (p_s - sb) + hb * kTcPBytes + r * 128;
+            // P_j (f16, 2 keys per 32-bit column) over the S_j columns in
+            // TMEM: the A operand of P.V_j
+            uint32_t pk[32];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {  // 8 keys per 16-byte chunk
-                float e[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    e[i] = fast_exp2(fmaf(__uint_as_float(sr[c >> 2][(c & 3) * 8 + i]), scale, -mu));
-                    ls[i & 3] += e[i];
-                }
-                uint4 pk;
-                pk.x = pack_f16(e[0], e[1]);
-                pk.y = pack_f16(e[2], e[3]);
-                pk.z = pack_f16(e[4], e[5]);
-                pk.w = pack_f16(e[6], e[7]);
-                *reinterpret_cast<uint4 *>(prow + ((c ^ (r & 7)) << 4)) = pk;
+            for (int c = 0; c < 32; ++c) {
+                const float e0 = fast_exp2(fmaf(__uint_as_float(sr[c >> 4][(2 * c) & 31]), scale, -mu));
+                const float e1 = fast_exp2(fmaf(__uint_as_float(sr[c >> 4][(2 * c + 1) & 31]), scale, -mu));
+                ls[c & 3] += e0 + e1;
+                pk[c] = pack_f16(e0, e1);
             }
+            tc_st32(s_t + b * kTcKeys, pk);
+            tc_wait_st();
             l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
-            fence_proxy_async();
             tc_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cta(p_full + 8 * hb);
