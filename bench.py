@@ -24,6 +24,8 @@ At N=1 the line also carries (rank 0 only):
 * ``mixed_trace`` -- config 5: mixed prefill/decode iterations (Alg. 1
   chunked prefill + decode, 32k prompts) on the 7 survivors, every rank
   emulated on this GPU;
+* ``cost_calibration`` -- the reference's iteration-time model fitted to
+  the per-rank times above (SURVEY 8f rank 4);
 * ``recovery`` -- config 4 microbenchmark (KV restore from the pinned host
   backup, weight shards) after 1-3 losses;
 * ``cpu_baseline`` -- the CPU oracle port on a bounded sample.
@@ -357,6 +359,66 @@ def mixed_trace(skip=24, n_iter=3, budget=2048, fail=7):
             "ranks": per_rank}
 
 
+# ------------------------------------------------- cost-model calibration --
+def cost_calibration(fstates, mixed, batch=64, ctx=4096, fails=(7, 3, 5), budget=2048):
+    """Fit the reference's iteration-time model (costmodel.py) to the
+    per-rank times measured above (C3 decode states, C5 mixed iterations):
+    SURVEY 8f rank 4.  Reports the B200 constants (seconds per unit), the
+    fit's RMS relative error per regime, and the error of the reference's
+    own FLOP constants at their default throughput for contrast."""
+    from paper_2511_14116_b200.core import load_config
+    from paper_2511_14116_b200.costmodel import (BatchWork, ChunkWork, CostParams, PlanCost,
+                                                 calibrate)
+    from paper_2511_14116_b200.placement import make_placement
+    from paper_2511_14116_b200.recovery import plan_weight_recovery
+    model, cluster = load_config(os.path.join(ROOT, "paper_2511_14116_b200", "data",
+                                              "llama70b.toml"))
+    ref = CostParams.from_model(model)
+    groups = {"decode": [], "mixed": []}
+    plan = make_placement("hybrid", model, range(8))
+    alive = list(range(8))
+    plans = {8: (plan, list(alive))}
+    for f in fails:
+        alive = [g for g in alive if g != f]
+        plan = plan_weight_recovery(model, plan, alive, "on_demand").target_plan("hybrid", model)
+        plans[len(alive)] = (plan, list(alive))
+    for st in fstates["states"]:
+        plan, al = plans[st["world"]]
+        routing = route(batch, al, ctx)
+        work = BatchWork([ChunkWork.decode(r, routing[r], ctx - 1) for r in range(batch)])
+        groups["decode"].append((PlanCost(plan, model, ref, cluster), work,
+                                 {r["rank"]: r["step_ms"] / 1e3 for r in st["ranks"]}))
+    plan, al = plans[7]
+    routing, steps, _ = mixed_iterations(sharegpt_trace(), al, budget, 24, 3)
+    for i, stb in enumerate(steps):
+        work = BatchWork([ChunkWork.prefill(r, routing[r], s0, n) for r, s0, n in stb.prefill] +
+                         [ChunkWork.decode(r, routing[r], pos) for r, pos in stb.decode])
+        groups["mixed"].append((PlanCost(plan, model, ref, cluster), work,
+                                {r["rank"]: r["iter_ms"][i] / 1e3 for r in mixed["ranks"]}))
+
+    def rms_err(params, samples):
+        errs = []
+        for pc, work, meas in samples:
+            pc2 = PlanCost(pc.plan, model, params, cluster)
+            pred = pc2.per_gpu_compute_time(work)
+            errs += [pred[g] / t - 1.0 for g, t in meas.items()]
+        return float(np.sqrt(np.mean(np.square(errs))))
+
+    import numpy as np
+    out = {"model": "reference costmodel.py (per-layer straggler max, linear in tokens / "
+                    "context tokens / token-shards), fitted per regime by NNLS on relative "
+                    "error; gpu_throughput = 1 (constants in seconds)"}
+    for name, samples in list(groups.items()) + [("both", groups["decode"] + groups["mixed"])]:
+        fit, err = calibrate(samples)
+        out[name] = {"attn_s_per_head_token": fit.attn_flop_per_head_token,
+                     "attn_s_per_head_ctx_token": fit.attn_flop_per_head_ctx_token,
+                     "ffn_s_per_token_shard": fit.ffn_flop_per_token_per_shard,
+                     "rms_rel_err": round(err, 4),
+                     "reference_flop_model_rms_rel_err": round(rms_err(ref, samples), 4),
+                     "samples": sum(len(m) for _, _, m in samples)}
+    return out
+
+
 # ------------------------------------------------------------ CPU oracle --
 def cpu_oracle_rate(qpk, ctx, seconds=8.0):
     """Items/s of the oracle port (float64 numpy decode of one (kv head,
@@ -552,6 +614,9 @@ def run_ours(args, world, rank, local_rank):
                                                     mlp=not args.no_mlp)
         if not args.skip_mixed:
             line["mixed_trace"] = mixed_trace()
+            if "failure_states" in line:
+                line["cost_calibration"] = cost_calibration(line["failure_states"],
+                                                            line["mixed_trace"])
         if not args.skip_recovery:
             try:
                 from paper_2511_14116_b200.recovery_exec import recovery_microbench

@@ -263,6 +263,41 @@ def gen_metrics():
     return {"jsonl": text, "summary": summ}
 
 
+def gen_costmodel():
+    """iteration_time / per_gpu_compute_time of the live cost model for
+    mixed batches on hybrid / cyclic / on-demand plans (costmodel.py)."""
+    from failsafe.costmodel import BatchWork, ChunkWork, CostParams, PlanCost
+    rng = random.Random(31)
+    model, cluster = load_config(os.path.join(DATA, "llama70b.toml"))
+    params = CostParams.from_model(model)
+    cases = []
+    for mode, world, fail in (("hybrid", 8, None), ("hybrid", 8, 7), ("cyclic", 7, None),
+                              ("hybrid", 6, None), ("naive", 5, None)):
+        plan = make_placement(mode, model, range(world))
+        alive = list(range(world))
+        if fail is not None:
+            alive.remove(fail)
+            plan = plan_weight_recovery(model, plan, alive, "on_demand").target_plan(mode, model)
+        for _ in range(4):
+            chunks = []
+            for r in range(rng.randint(1, 40)):
+                g = rng.choice(alive)
+                if rng.random() < 0.3:
+                    chunks.append(["prefill", r, g, rng.randint(0, 5000), rng.randint(1, 512)])
+                else:
+                    chunks.append(["decode", r, g, rng.randint(1, 8000)])
+            work = BatchWork([ChunkWork.prefill(*c[1:]) if c[0] == "prefill"
+                              else ChunkWork.decode(*c[1:]) for c in chunks])
+            pc = PlanCost(plan, model, params, cluster)
+            cases.append({"mode": mode, "world": world, "fail": fail, "chunks": chunks,
+                          "iteration_time": pc.iteration_time(work),
+                          "per_gpu": {str(g): t for g, t in pc.per_gpu_compute_time(work).items()}})
+    p = params
+    return {"params": [p.attn_flop_per_head_token, p.attn_flop_per_head_ctx_token,
+                       p.ffn_flop_per_token_per_shard, p.gpu_throughput],
+            "allreduce": [cluster.allreduce_alpha, cluster.allreduce_beta], "cases": cases}
+
+
 def toy_model(L, H, shards, qpk=1):
     return ModelSpec(num_layers=L, num_kv_heads=H, num_q_heads=H * qpk, head_dim=8,
                      hidden_dim=32, ffn_intermediate_dim=96, ffn_num_shards=shards)
@@ -434,7 +469,8 @@ def main():
     os.makedirs(OUT, exist_ok=True)
     gens = (("placement", gen_placement), ("routing", gen_routing),
             ("recovery", gen_recovery), ("forward", gen_forward), ("decode", gen_decode),
-            ("batches", gen_batches), ("prefill", gen_prefill), ("metrics", gen_metrics))
+            ("batches", gen_batches), ("prefill", gen_prefill), ("metrics", gen_metrics),
+            ("costmodel", gen_costmodel))
     only = sys.argv[1:]
     for name, fn in gens:
         if only and name not in only:
