@@ -71,7 +71,7 @@ def _expected(work, kv, q, lens, n_rows):
     return out
 
 
-@pytest.mark.parametrize("qpk", [1, 4, 8])
+@pytest.mark.parametrize("qpk", [1, 3, 4, 6, 8])
 @pytest.mark.parametrize("config", [0, 3, 7, 9])
 def test_decode_hybrid_rank_ragged(qpk, config):
     """Hybrid N=7 rank: 1 TP head for all requests + 1 DP head for routed

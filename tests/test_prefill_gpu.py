@@ -91,7 +91,7 @@ VARIANTS = [0, 1, 2]
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
-@pytest.mark.parametrize("qpk", [1, 3, 4, 8])
+@pytest.mark.parametrize("qpk", [1, 2, 3, 4, 5, 6, 7, 8])
 def test_prefill_ragged(qpk, variant):
     """Ragged chunks: fresh prompts, continuation chunks at page and
     non-page boundaries, 1-token chunks, a long prefix, an empty item."""
