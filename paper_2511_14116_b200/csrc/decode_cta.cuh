@@ -280,44 +280,20 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_cta_kernel(const DecodeP
                 for (int64_t s = clo; s <= chi; ++s) nseg += warp_live(s, C, P);
             }
             if (s_prev == nseg - 1) {
-                // last CTA of the item: merge its (up to ~all-CTA) partials
-                // with every warp -- warp w takes segments clo+w, clo+w+WARPS,
-                // ... for all queries (8 independent float4 loads per
-                // segment), then the warps' sums are reduced in smem.  A
-                // one-warp serial merge costs ~40 us when one long item
-                // spans all 148 CTAs (batch-1 decode).
+                // last CTA of the item: merge its (up to ~all-CTA) partials.
+                // Warp w streams segments clo+w, clo+w+WARPS, ... issuing each
+                // segment's lse and O loads together and folding them into a
+                // running log-sum-exp (m, l, acc) per query -- one L2 round
+                // trip for the usual <= WARPS segments -- then the warps'
+                // states are combined in smem.
                 __threadfence();
                 const bool all_live = P >= C;
                 const int qpk = p.qpk;
-                float mx[FS_MAX_Q_PER_KV];
-#pragma unroll
-                for (int q = 0; q < FS_MAX_Q_PER_KV; ++q) mx[q] = -INFINITY;
-                for (int64_t s = clo + threadIdx.x; s <= chi; s += NT) {
-                    if (!all_live && !warp_live(s, C, P)) continue;
-#pragma unroll
-                    for (int q = 0; q < FS_MAX_Q_PER_KV; ++q)
-                        if (q < qpk) mx[q] = fmaxf(mx[q], __ldcg(p.part_lse + (item + s) * qpk + q));
-                }
-                float *slot = merge + warp * kSlot;
-#pragma unroll
-                for (int q = 0; q < FS_MAX_Q_PER_KV; ++q) {
-#pragma unroll
-                    for (int sh = 1; sh < 32; sh <<= 1)
-                        mx[q] = fmaxf(mx[q], __shfl_xor_sync(0xffffffffu, mx[q], sh));
-                    if (lane == 0) slot[q] = mx[q];
-                }
-                named_bar(1, NT);
-#pragma unroll
-                for (int q = 0; q < FS_MAX_Q_PER_KV; ++q) {
-                    float m = -INFINITY;
-#pragma unroll
-                    for (int k = 0; k < WARPS; ++k) m = fmaxf(m, merge[k * kSlot + q]);
-                    mx[q] = m;
-                }
-                float lw[FS_MAX_Q_PER_KV];
+                float mw[FS_MAX_Q_PER_KV], lw[FS_MAX_Q_PER_KV];
                 float4 acc[FS_MAX_Q_PER_KV];
 #pragma unroll
                 for (int q = 0; q < FS_MAX_Q_PER_KV; ++q) {
+                    mw[q] = -INFINITY;
                     lw[q] = 0.f;
                     acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
                 }
@@ -325,49 +301,59 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_cta_kernel(const DecodeP
                     if (!all_live && !warp_live(s, C, P)) continue;
                     const float *ls = p.part_lse + (item + s) * qpk;
                     const float4 *os = reinterpret_cast<const float4 *>(p.part_o + (item + s) * qpk * kHeadDim);
+                    float lv[FS_MAX_Q_PER_KV];
                     float4 v[FS_MAX_Q_PER_KV];
-                    float wk[FS_MAX_Q_PER_KV];
 #pragma unroll
                     for (int q = 0; q < FS_MAX_Q_PER_KV; ++q) {
                         if (q < qpk) {
-                            wk[q] = __ldcg(ls + q);
+                            lv[q] = __ldcg(ls + q);
                             v[q] = __ldcg(os + q * (kHeadDim / 4) + lane);
                         }
                     }
 #pragma unroll
                     for (int q = 0; q < FS_MAX_Q_PER_KV; ++q) {
                         if (q < qpk) {
-                            const float w = fast_exp2(wk[q] - mx[q]);
-                            lw[q] += w;
-                            acc[q].x += w * v[q].x;
-                            acc[q].y += w * v[q].y;
-                            acc[q].z += w * v[q].z;
-                            acc[q].w += w * v[q].w;
+                            const float mn = fmaxf(mw[q], lv[q]);
+                            const float a0 = fast_exp2(mw[q] - mn), a1 = fast_exp2(lv[q] - mn);
+                            mw[q] = mn;
+                            lw[q] = lw[q] * a0 + a1;
+                            acc[q].x = acc[q].x * a0 + v[q].x * a1;
+                            acc[q].y = acc[q].y * a0 + v[q].y * a1;
+                            acc[q].z = acc[q].z * a0 + v[q].z * a1;
+                            acc[q].w = acc[q].w * a0 + v[q].w * a1;
                         }
                     }
                 }
-                named_bar(1, NT);  // everyone has read the maxima
+                float *slot = merge + warp * kSlot;
                 float *om = slot + 2 * FS_MAX_Q_PER_KV;
 #pragma unroll
                 for (int q = 0; q < FS_MAX_Q_PER_KV; ++q) {
                     if (q < qpk) {
-                        if (lane == 0) slot[FS_MAX_Q_PER_KV + q] = lw[q];
+                        if (lane == 0) {
+                            slot[q] = mw[q];
+                            slot[FS_MAX_Q_PER_KV + q] = lw[q];
+                        }
                         *reinterpret_cast<float4 *>(om + q * kMergeStride + lane * 4) = acc[q];
                     }
                 }
                 named_bar(1, NT);
                 for (int q = warp; q < qpk; q += WARPS) {
+                    float M = -INFINITY;
+#pragma unroll
+                    for (int k = 0; k < WARPS; ++k) M = fmaxf(M, merge[k * kSlot + q]);
                     float L = 0.f;
                     float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                     for (int k = 0; k < WARPS; ++k) {
-                        L += merge[k * kSlot + FS_MAX_Q_PER_KV + q];
+                        const float mk = merge[k * kSlot + q];
+                        const float wk = mk == -INFINITY ? 0.f : fast_exp2(mk - M);
+                        L += wk * merge[k * kSlot + FS_MAX_Q_PER_KV + q];
                         const float4 t = *reinterpret_cast<const float4 *>(
                             merge + k * kSlot + 2 * FS_MAX_Q_PER_KV + q * kMergeStride + lane * 4);
-                        sum.x += t.x;
-                        sum.y += t.y;
-                        sum.z += t.z;
-                        sum.w += t.w;
+                        sum.x += wk * t.x;
+                        sum.y += wk * t.y;
+                        sum.z += wk * t.z;
+                        sum.w += wk * t.w;
                     }
                     const float inv = 1.f / L;
                     const int64_t ob = (int64_t)p.item_ooff[item] + q * kHeadDim + lane * 4;
