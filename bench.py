@@ -11,8 +11,9 @@ attention output).  One JSON line on rank 0.
 
 A *step* = one decode token for all 64 requests through every layer:
 fused QKV GEMM (cuBLAS) -> ONE fs_decode_attention launch (KV append + paged
-GQA decode + split merge) -> output projection -> exchange (NCCL all-reduce
-when N>1) -> residual -> TP MLP partial over the rank's FFN shards (gate/up
+GQA decode + split merge) -> output projection -> exchange + residual (N>1:
+one fs_ar_residual kernel over IPC-mapped peer buffers, ``--exchange nccl``
+for an NCCL all-reduce) -> TP MLP partial over the rank's FFN shards (gate/up
 GEMM, fs_swiglu, down GEMM) -> exchange -> residual (``--no-mlp``: attention
 sublayer only).  The whole step is one CUDA-graph replay.  The KV working set
 (34 GB at N=1) is far larger than L2, so no flush is needed between steps.
@@ -49,6 +50,7 @@ METRIC = ("decode tokens/s at 8→7→6→5 B200 (fraction of HBM roofline); "
 UNIT = "tokens/s"
 KV_UNIT = 512  # bytes per (kv head, token): K+V, head_dim 128, bf16 (core.py:101-103)
 GEMM_BACKEND = "cublas"  # --gemm: projections via cuBLAS or the tcgen05 skinny GEMM
+EXCHANGE = "fused"  # --exchange (N>1): fs_ar_residual over peer memory, or NCCL all-reduce
 
 
 def measured_peaks():
@@ -142,11 +144,13 @@ def build_rank(model, plan, rank, routing, batch, ctx, group, config, seed=0, ml
     owner = owner_array(plan, model.num_kv_heads)
     shards = [plan.ffn.owner[s] for s in range(plan.ffn.num_shards)]
     eng = HybridDecodeRank(model, owner, rank, routing, batch, ctx, group=group, seed=seed,
-                           config=config, mlp=mlp, shard_owner=shards, gemm=GEMM_BACKEND)
+                           config=config, mlp=mlp, shard_owner=shards, gemm=GEMM_BACKEND,
+                           exchange=EXCHANGE)
     eng.set_lengths([ctx] * batch)
     eng.fill_random_kv(seed + 17 * rank)
     eng.x.copy_(torch.randn_like(eng.x, dtype=torch.float32).to(torch.bfloat16))
-    if os.environ.get("FS_BENCH_SHARED_GPU") != "1":  # gloo collectives are not capturable
+    # gloo collectives are not capturable (the fused exchange is)
+    if os.environ.get("FS_BENCH_SHARED_GPU") != "1" or eng.xchg is not None or group is None:
         eng.capture()
     return eng
 
@@ -510,8 +514,9 @@ def run_reference(args, world, rank):
 def workload_config(model, world, batch, ctx):
     return {"workload": "C2 Llama-3-8B-shaped hybrid-attention decode step, all 32 layers: "
                         "QKV GEMM, fused KV-append + paged GQA decode, O GEMM, TP MLP "
-                        "partial (gate/up GEMM, swiglu, down GEMM); NCCL all-reduce of the "
-                        "attention and MLP partials when N>1",
+                        "partial (gate/up GEMM, swiglu, down GEMM); when N>1 the attention and MLP "
+                        "partials are exchanged by fs_ar_residual (ordered sum + residual in one "
+                        "kernel over IPC-mapped peer buffers; --exchange nccl: NCCL all-reduce)",
             "layers": model.num_layers, "q_heads": model.num_q_heads,
             "kv_heads": model.num_kv_heads, "head_dim": model.head_dim,
             "hidden": model.hidden_dim, "batch": batch, "ctx": ctx, "world": world,
@@ -650,6 +655,9 @@ def main():
                     help="skip the config-5 mixed prefill/decode trace section")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--gemm", default="cublas", choices=("cublas", "tcgen05"))
+    ap.add_argument("--exchange", default="fused", choices=("fused", "nccl"),
+                    help="N>1 exchange: one fs_ar_residual kernel over IPC-mapped peer "
+                         "buffers (default) or an NCCL all-reduce + add")
     ap.add_argument("--no-mlp", action="store_true",
                     help="attention sublayer only (no TP MLP partial / MLP all-reduce)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
@@ -657,8 +665,9 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
-    global GEMM_BACKEND
+    global GEMM_BACKEND, EXCHANGE
     GEMM_BACKEND = args.gemm
+    EXCHANGE = args.exchange
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

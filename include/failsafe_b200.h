@@ -34,6 +34,9 @@
  *                          (scheduler.build_prefill_batch) refexec.py:85-103,
  *                                                          scheduler.py:189-245
  *   fs_plan_prefill_tiles <- (new) host tile/split planner of that launch
+ *   fs_ar_residual      <- the ordered sum of parallel_forward's per-rank
+ *                          partials (+ residual), refexec.py:283-307, as one
+ *                          kernel over IPC-mapped peer memory
  *   fs_kv_write / fs_kv_read <- (new) KV append into / read from pages
  *   fs_pages_gather     <- recovery.advance_backup executed as an incremental
  *                          page copy to pinned host       recovery.py:193-247
@@ -273,6 +276,27 @@ int fs_swiglu(const void *h, int64_t rows, int64_t cols, int64_t ld, void *out,
 int fs_fill_normal(void *out, int64_t rows, int64_t cols, int64_t ld,
                    const int32_t *row_map, int64_t row_off, const int32_t *col_map,
                    int64_t col_off, uint64_t seed, uint64_t salt, float scale, void *stream);
+
+/* ---- the exchange: ordered-sum all-reduce + residual over peer memory ----
+ * (refexec.py:283-307).  Each rank owns symmetric buffers of
+ * fs_ar_buffer_bytes(max_elems) bytes (fs_ar_alloc: zeroed cudaMalloc),
+ * shares them with CUDA IPC (fs_ar_ipc_handle -> 64-byte handle ->
+ * fs_ar_ipc_open on every peer) and writes its bf16 partial to the first
+ * n elements of its own buffer.  fs_ar_residual then signals / waits on the
+ * peers' flags and does x[i] += bf16(sum over ranks 0..world-1, in order,
+ * in fp32, of partial_r[i]) in ONE launch (peers[r] = buffer of rank r as
+ * mapped in this process, data_bytes = the buffer's flag offset =
+ * fs_ar_buffer_bytes(max_elems) - 256).  Consecutive exchanges must
+ * alternate between two buffers.  Traps (no hang) if a peer never arrives. */
+#define FS_AR_MAX_WORLD 16
+int64_t fs_ar_buffer_bytes(int64_t max_elems);
+int fs_ar_alloc(int device, int64_t bytes, void **ptr);
+int fs_ar_free(void *ptr);
+int fs_ar_ipc_handle(void *ptr, void *handle64);
+int fs_ar_ipc_open(const void *handle64, void **ptr);
+int fs_ar_ipc_close(void *ptr);
+int fs_ar_residual(void *const *peers, int32_t rank, int32_t world, int64_t n,
+                   int64_t data_bytes, void *x, int32_t ctas, void *stream);
 
 /* K7: enable peer access (idempotent) and peer copy */
 int fs_enable_peer(int device, int peer);

@@ -21,6 +21,7 @@ PAGE_TOKENS = 16
 HEAD_DIM = 128
 PAGE_BYTES = 8192
 MAX_Q_PER_KV = 8
+FS_AR_MAX_WORLD = 16
 MODES = {"naive": 0, "cyclic": 1, "hybrid": 2}
 
 _i32p = C.POINTER(C.c_int32)
@@ -99,6 +100,14 @@ _SIGS = {
     "fs_fill_normal": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
                                  C.c_int64, C.c_void_p, C.c_int64, C.c_uint64, C.c_uint64,
                                  C.c_float, C.c_void_p]),
+    "fs_ar_buffer_bytes": (C.c_int64, [C.c_int64]),
+    "fs_ar_alloc": (C.c_int, [C.c_int, C.c_int64, C.POINTER(C.c_void_p)]),
+    "fs_ar_free": (C.c_int, [C.c_void_p]),
+    "fs_ar_ipc_handle": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "fs_ar_ipc_open": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "fs_ar_ipc_close": (C.c_int, [C.c_void_p]),
+    "fs_ar_residual": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int64,
+                                 C.c_int64, C.c_void_p, C.c_int32, C.c_void_p]),
     "fs_enable_peer": (C.c_int, [C.c_int, C.c_int]),
     "fs_copy_peer": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int64,
                                C.c_void_p]),

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libfailsafe_b200.so")
-SOURCES = ["abi.cpp", "planner.cpp", "decode.cu", "kvcache.cu", "mlp.cu", "gemm.cu", "prefill.cu"]
+SOURCES = ["abi.cpp", "planner.cpp", "decode.cu", "kvcache.cu", "mlp.cu", "gemm.cu", "prefill.cu", "allreduce.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -1,0 +1,127 @@
+"""The exchange step over peer memory (fs_ar_residual).
+
+``parallel_forward`` sums the per-rank attention / FFN partials in ascending
+rank order and adds them to the residual stream (refexec.py:283-307).  On
+B200s in one NVSwitch domain that exchange is ONE kernel per sub-layer: each
+rank's projection GEMM writes its partial straight into a symmetric buffer
+that every peer has mapped (CUDA IPC over NVLink), and ``fs_ar_residual``
+signals the peers, waits for them, and does ``x += bf16(sum_r partial_r)``
+reading the partials in rank order -- the reference's exact ordered sum,
+bit-identical on every rank, with no NCCL launch and no separate residual
+add.  Two buffers alternate between consecutive exchanges (the kernel's
+flag protocol needs no second barrier then).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+import torch.distributed as dist
+
+from . import _native as N
+from .core import SimulationError, ValidationError
+
+
+class _DeviceArray:
+    """``__cuda_array_interface__`` view of raw device memory (uint16)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<u2", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class FusedExchange:
+    """Two symmetric exchange buffers of this rank and their peer mappings.
+
+    ``group``: the torch.distributed group of the alive ranks (any backend;
+    used once to swap IPC handles); ``max_elems``: largest partial (bf16
+    elements, e.g. batch x hidden).  All ranks must construct it together.
+    """
+
+    def __init__(self, group, max_elems: int, device=None, check: bool = True):
+        self.device = torch.device(device if device is not None else "cuda")
+        dev = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if self.world > N.FS_AR_MAX_WORLD:
+            raise ValidationError(f"fused exchange supports up to {N.FS_AR_MAX_WORLD} ranks")
+        self.max_elems = int(max_elems) + (-int(max_elems)) % 8
+        self.nbytes = int(N.lib.fs_ar_buffer_bytes(self.max_elems))
+        self.data_bytes = self.nbytes - 256
+        self._own, self._opened = [], []
+        handles = []
+        for _ in range(2):
+            p = C.c_void_p()
+            N.check(N.lib.fs_ar_alloc(dev, self.nbytes, C.byref(p)), "fs_ar_alloc")
+            self._own.append(p.value)
+            h = (C.c_uint8 * 64)()
+            N.check(N.lib.fs_ar_ipc_handle(C.c_void_p(p.value), h), "fs_ar_ipc_handle")
+            handles.append(bytes(h))
+        every = [None] * self.world
+        dist.all_gather_object(every, handles, group=group)
+        self.peers = []
+        for i in range(2):
+            arr = (C.c_void_p * self.world)()
+            for r in range(self.world):
+                if r == self.rank:
+                    arr[r] = self._own[i]
+                    continue
+                q = C.c_void_p()
+                h = (C.c_uint8 * 64).from_buffer_copy(every[r][i])
+                N.check(N.lib.fs_ar_ipc_open(h, C.byref(q)), "fs_ar_ipc_open")
+                self._opened.append(q.value)
+                arr[r] = q.value
+            self.peers.append(arr)
+        self._views = [torch.as_tensor(_DeviceArray(p, self.max_elems), device=self.device)
+                       .view(torch.bfloat16) for p in self._own]
+        dist.barrier(group=group)
+        if check:
+            self._self_check()
+
+    def partial(self, i: int, shape) -> torch.Tensor:
+        """This rank's partial buffer ``i`` (0/1) as a bf16 tensor of ``shape``
+        -- the projection GEMM's ``out``."""
+        n = 1
+        for s in shape:
+            n *= int(s)
+        if n > self.max_elems:
+            raise ValidationError("partial larger than the exchange buffer")
+        return self._views[i][:n].view(*shape)
+
+    def reduce_residual(self, i: int, x: torch.Tensor) -> None:
+        """``x += bf16(sum over ranks, in rank order, of partial_r)`` where
+        partial_r is rank r's buffer ``i`` (its first ``x.numel()`` elements)."""
+        if x.dtype != torch.bfloat16 or not x.is_contiguous() or x.numel() % 8:
+            raise ValidationError("x must be contiguous bf16 with a multiple of 8 elements")
+        st = torch.cuda.current_stream(self.device).cuda_stream
+        N.check(N.lib.fs_ar_residual(self.peers[i], self.rank, self.world, x.numel(),
+                                     self.data_bytes, C.c_void_p(x.data_ptr()), 0,
+                                     C.c_void_p(st)), "fs_ar_residual")
+
+    def _self_check(self) -> None:
+        """One exchange on each buffer with rank-keyed data, checked against
+        the ordered sum every rank can recompute."""
+        n = min(self.max_elems, 4096)
+        for i in range(2):
+            parts = [torch.randn(n, generator=torch.Generator().manual_seed(1000 * r + i))
+                     .to(torch.bfloat16) for r in range(self.world)]
+            self.partial(i, (n,)).copy_(parts[self.rank].to(self.device))
+            x = torch.ones(n, dtype=torch.bfloat16, device=self.device)
+            torch.cuda.current_stream(self.device).synchronize()
+            self.reduce_residual(i, x)
+            total = torch.zeros(n)
+            for p in parts:
+                total += p.float()
+            want = (torch.ones(n, dtype=torch.bfloat16).float() +
+                    total.to(torch.bfloat16).float()).to(torch.bfloat16)
+            if not torch.equal(x.cpu(), want):
+                raise SimulationError(f"fused exchange self-check failed on rank {self.rank}")
+
+    def close(self) -> None:
+        torch.cuda.synchronize(self.device)
+        for p in self._opened:
+            N.lib.fs_ar_ipc_close(C.c_void_p(p))
+        for p in self._own:
+            N.lib.fs_ar_free(C.c_void_p(p))
+        self._opened, self._own = [], []

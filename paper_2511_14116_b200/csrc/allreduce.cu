@@ -1,0 +1,185 @@
+// The exchange step of the hybrid decode step (the reference's ordered sum of
+// the per-rank partials, refexec.py:283-307) as ONE kernel over peer memory:
+// every rank's projection GEMM writes its partial straight into a symmetric
+// buffer (cudaMalloc'd, shared with the peers by CUDA IPC, mapped over
+// NVLink / NVSwitch), and fs_ar_residual then
+//   1. publishes "my partial is ready" to every peer (a release store of the
+//      buffer's use counter into each peer's flag slot for this rank),
+//   2. waits until every peer's flag reached this use (acquire loads),
+//   3. reads the partials of all ranks IN RANK ORDER, sums them in fp32,
+//      rounds once to bf16 and adds them to the residual stream x in place:
+//      x += bf16(sum_r partial_r) -- the reference's exact ordered sum, and
+//      bit-identical on every rank (unlike a ring / tree all-reduce).
+// No second barrier: a caller alternates two buffers between consecutive
+// exchanges (attention / MLP), and a rank can only rewrite buffer A after
+// its exchange on buffer B passed its barrier, i.e. after every peer
+// finished reading A.  The use counter and flags live in device memory, so
+// the launch is CUDA-graph capturable.  A peer that never arrives makes the
+// kernel trap after 5 s instead of hanging the GPU.
+#include <cuda_bf16.h>
+
+#include <cstring>
+
+#include "common.cuh"
+
+namespace fs {
+
+constexpr int64_t kSpinNs = 5000000000LL;  // 5 s
+
+struct ArParams {
+    uint8_t *peer[FS_AR_MAX_WORLD];
+    int32_t rank, world;
+    int64_t n;          // bf16 elements (multiple of 8)
+    int64_t data_bytes; // offset of the flag area inside every buffer
+    __nv_bfloat16 *x;
+};
+
+__device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long now_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// flag area of a buffer: [FS_AR_MAX_WORLD] arrival flags, then the use
+// counter and the CTA-done counter
+__device__ __forceinline__ uint32_t *flags_of(uint8_t *buf, int64_t data_bytes) {
+    return reinterpret_cast<uint32_t *>(buf + data_bytes);
+}
+
+__global__ void __launch_bounds__(256) ar_residual_kernel(const ArParams p) {
+    __shared__ uint32_t s_use;
+    uint32_t *mine = flags_of(p.peer[p.rank], p.data_bytes);
+    uint32_t *use_ctr = mine + FS_AR_MAX_WORLD, *done_ctr = use_ctr + 1;
+    if (threadIdx.x == 0) s_use = *reinterpret_cast<volatile uint32_t *>(use_ctr) + 1u;
+    __syncthreads();
+    const uint32_t use = s_use;
+    if (blockIdx.x == 0 && threadIdx.x < p.world) {
+        __threadfence_system();  // my partial (written by the GEMM) before the flag
+        st_release_sys(flags_of(p.peer[threadIdx.x], p.data_bytes) + p.rank, use);
+    }
+    if (threadIdx.x < p.world) {
+        const unsigned long long t0 = now_ns();
+        while (ld_acquire_sys(mine + threadIdx.x) < use) {
+            if (now_ns() - t0 > (unsigned long long)kSpinNs) asm volatile("trap;");
+        }
+    }
+    __syncthreads();
+    const int64_t n8 = p.n / 8;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int r = 0; r < p.world; ++r) {  // rank order: deterministic everywhere
+            const uint4 v = __ldcv(reinterpret_cast<const uint4 *>(p.peer[r]) + i);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                acc[2 * k] += __uint_as_float(w[k] << 16);
+                acc[2 * k + 1] += __uint_as_float(w[k] & 0xffff0000u);
+            }
+        }
+        uint4 *xp = reinterpret_cast<uint4 *>(p.x) + i;
+        uint4 xv = *xp;
+        uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            // x + bf16(sum): the reference's residual with the rounded total
+            const uint32_t t = pack_bf16(acc[2 * k], acc[2 * k + 1]);
+            const float lo = __uint_as_float(xw[k] << 16) + __uint_as_float(t << 16);
+            const float hi = __uint_as_float(xw[k] & 0xffff0000u) + __uint_as_float(t & 0xffff0000u);
+            xw[k] = pack_bf16(lo, hi);
+        }
+        *xp = make_uint4(xw[0], xw[1], xw[2], xw[3]);
+    }
+    // the last CTA out advances the use counter for the next exchange on
+    // this buffer (read by this rank only, after this kernel)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(done_ctr, 1u) == gridDim.x - 1) {
+            *use_ctr = use;
+            *done_ctr = 0;
+        }
+    }
+}
+
+}  // namespace fs
+
+using namespace fs;
+
+extern "C" int64_t fs_ar_buffer_bytes(int64_t max_elems) {
+    if (max_elems < 0) return -1;
+    const int64_t data = ((max_elems * 2 + 255) / 256) * 256;
+    return data + 256;  // flags, use counter, done counter
+}
+
+extern "C" int fs_ar_alloc(int device, int64_t bytes, void **ptr) {
+    FS_CHECK_ARG(ptr && bytes > 0, "bad arguments");
+    int prev = 0;
+    FS_CUDA(cudaGetDevice(&prev));
+    FS_CUDA(cudaSetDevice(device));
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, (size_t)bytes);
+    if (e == cudaSuccess) e = cudaMemset(p, 0, (size_t)bytes);
+    cudaSetDevice(prev);
+    FS_CUDA(e);
+    *ptr = p;
+    return FS_OK;
+}
+
+extern "C" int fs_ar_free(void *ptr) {
+    if (ptr) FS_CUDA(cudaFree(ptr));
+    return FS_OK;
+}
+
+extern "C" int fs_ar_ipc_handle(void *ptr, void *handle) {
+    FS_CHECK_ARG(ptr && handle, "null pointer");
+    cudaIpcMemHandle_t h;
+    FS_CUDA(cudaIpcGetMemHandle(&h, ptr));
+    memcpy(handle, &h, sizeof(h));
+    return FS_OK;
+}
+
+extern "C" int fs_ar_ipc_open(const void *handle, void **ptr) {
+    FS_CHECK_ARG(ptr && handle, "null pointer");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    FS_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return FS_OK;
+}
+
+extern "C" int fs_ar_ipc_close(void *ptr) {
+    if (ptr) FS_CUDA(cudaIpcCloseMemHandle(ptr));
+    return FS_OK;
+}
+
+extern "C" int fs_ar_residual(void *const *peers, int32_t rank, int32_t world, int64_t n,
+                              int64_t data_bytes, void *x, int32_t ctas, void *stream) {
+    FS_CHECK_ARG(world >= 1 && world <= FS_AR_MAX_WORLD, "world must be in [1, %d]", FS_AR_MAX_WORLD);
+    FS_CHECK_ARG(rank >= 0 && rank < world, "rank out of range");
+    FS_CHECK_ARG(n >= 0 && n % 8 == 0 && n * 2 <= data_bytes, "n must be a multiple of 8 that fits");
+    FS_CHECK_ARG(peers && x && (reinterpret_cast<uintptr_t>(x) & 15) == 0, "bad pointers");
+    ArParams prm = {};
+    for (int r = 0; r < world; ++r) {
+        FS_CHECK_ARG(peers[r] && (reinterpret_cast<uintptr_t>(peers[r]) & 255) == 0,
+                     "peer buffer %d missing or misaligned", r);
+        prm.peer[r] = static_cast<uint8_t *>(peers[r]);
+    }
+    prm.rank = rank;
+    prm.world = world;
+    prm.n = n;
+    prm.data_bytes = data_bytes;
+    prm.x = static_cast<__nv_bfloat16 *>(x);
+    const int64_t need = (n / 8 + 255) / 256;
+    int grid = ctas > 0 ? ctas : 148;
+    if (grid > need) grid = (int)(need > 0 ? need : 1);
+    ar_residual_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(prm);
+    return cuda_status(cudaGetLastError(), "ar_residual_kernel launch");
+}

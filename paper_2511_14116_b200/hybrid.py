@@ -116,7 +116,7 @@ class HybridDecodeRank:
     def __init__(self, model: ModelSpec, owner, rank: int, routing, batch: int, capacity: int,
                  device=None, seed: int = 0, group=None, page_order: str = "contiguous",
                  config: int = 0, mlp: bool = False, shard_owner=None, gemm: str = "cublas",
-                 request_capacity=None):
+                 request_capacity=None, exchange: str = "nccl"):
         if model.head_dim != N.HEAD_DIM:
             raise ValidationError(f"head_dim must be {N.HEAD_DIM} for the CUDA path")
         self.model = model
@@ -168,6 +168,16 @@ class HybridDecodeRank:
             self.act = torch.empty((batch, C), dtype=torch.bfloat16, device=dev)
         if gemm not in ("cublas", "tcgen05"):
             raise ValidationError(f"unknown gemm backend {gemm!r}")
+        if exchange not in ("nccl", "fused"):
+            raise ValidationError(f"unknown exchange {exchange!r}")
+        # exchange "fused": the projection GEMMs write their partials into
+        # IPC-shared buffers and fs_ar_residual does the ordered sum + the
+        # residual in one kernel over peer memory (collective.py)
+        self.exchange = exchange if group is not None else "nccl"
+        self.xchg = None
+        if self.exchange == "fused":
+            from .collective import FusedExchange
+            self.xchg = FusedExchange(group, batch * model.hidden_dim, self.device)
         self.gemm = gemm
         if gemm == "tcgen05":
             self._use_skinny()
@@ -278,6 +288,22 @@ class HybridDecodeRank:
                     torch.matmul(x, self.w_gu[layer], out=self.h)
                     self._swiglu()
                     x.addmm_(self.act, self.w_d[layer])              # x += act Wd
+            elif self.xchg is not None:
+                # buffers alternate between consecutive exchanges
+                ia, im = (0, 1) if self.mlp else (layer & 1, None)
+                torch.matmul(x, self.wqkv[layer], out=self.qkv)
+                self.cache.decode_layer_fused(layer, self.qkv, self.o)
+                torch.matmul(o2, self.wo[layer], out=self.xchg.partial(ia, x.shape))
+                self.xchg.reduce_residual(ia, x)                     # x += sum_r part_r
+                if self.mlp:
+                    part = self.xchg.partial(im, x.shape)
+                    if len(self.ffn_cols):
+                        torch.matmul(x, self.w_gu[layer], out=self.h)
+                        self._swiglu()
+                        torch.matmul(self.act, self.w_d[layer], out=part)
+                    else:
+                        part.zero_()
+                    self.xchg.reduce_residual(im, x)
             else:
                 self.attention_partial(layer)
                 torch.distributed.all_reduce(self.part, group=self.group)
@@ -294,7 +320,10 @@ class HybridDecodeRank:
         has_mlp = self.mlp and len(self.ffn_cols)
         if self.gemm == "tcgen05":
             return self.model.num_layers * (5 if has_mlp else 3)
-        return self.model.num_layers * (2 if has_mlp else 1)
+        n = self.model.num_layers * (2 if has_mlp else 1)
+        if self.xchg is not None:  # one fs_ar_residual per exchange
+            n += self.model.num_layers * (2 if self.mlp else 1)
+        return n
 
     def weight_bytes(self) -> int:
         if self.gemm == "tcgen05":
