@@ -116,7 +116,7 @@ class HybridDecodeRank:
     def __init__(self, model: ModelSpec, owner, rank: int, routing, batch: int, capacity: int,
                  device=None, seed: int = 0, group=None, page_order: str = "contiguous",
                  config: int = 0, mlp: bool = False, shard_owner=None, gemm: str = "cublas",
-                 request_capacity=None, exchange: str = "nccl"):
+                 request_capacity=None, exchange: str = "nccl", exchange_elems: int = None):
         if model.head_dim != N.HEAD_DIM:
             raise ValidationError(f"head_dim must be {N.HEAD_DIM} for the CUDA path")
         self.model = model
@@ -177,7 +177,8 @@ class HybridDecodeRank:
         self.xchg = None
         if self.exchange == "fused":
             from .collective import FusedExchange
-            self.xchg = FusedExchange(group, batch * model.hidden_dim, self.device)
+            self.xchg = FusedExchange(group, exchange_elems or batch * model.hidden_dim,
+                                      self.device)
         self.gemm = gemm
         if gemm == "tcgen05":
             self._use_skinny()

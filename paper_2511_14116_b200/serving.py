@@ -221,14 +221,15 @@ class HybridServingRank(HybridDecodeRank):
 
     def __init__(self, model, owner, rank: int, routing, request_capacity, max_tokens: int,
                  device=None, seed: int = 0, group=None, mlp: bool = True, shard_owner=None,
-                 config: int = 0, page_order: str = "contiguous"):
+                 config: int = 0, page_order: str = "contiguous", exchange: str = "nccl"):
         cap = np.asarray(request_capacity, dtype=np.int64)
         if cap.ndim != 1 or cap.size == 0 or cap.min() < 1:
             raise ValidationError("request_capacity must list >= 1 token per request")
         super().__init__(model, owner, rank, routing, int(cap.size), int(cap.max()),
                          device=device, seed=seed, group=group, page_order=page_order,
                          config=config, mlp=mlp, shard_owner=shard_owner,
-                         request_capacity=cap)
+                         request_capacity=cap, exchange=exchange,
+                         exchange_elems=int(max_tokens) * model.hidden_dim)
         self.request_capacity = cap
         self.max_tokens = int(max_tokens)
         S, hd, qpk, hid = self.n_slots, model.head_dim, self.qpk, model.hidden_dim
@@ -309,6 +310,8 @@ class HybridServingRank(HybridDecodeRank):
         xs = self.x_s[:T]
         if x is not None:
             xs.copy_(x, non_blocking=True)
+        if self.xchg is not None:
+            return self._serve_fused(plan, xs)
         for layer in range(self.model.num_layers):
             part = self.serve_attention_partial(layer, plan)
             if self.group is not None:
@@ -319,6 +322,28 @@ class HybridServingRank(HybridDecodeRank):
                 if self.group is not None:
                     torch.distributed.all_reduce(part, group=self.group)
                 xs.add_(part)
+        return xs
+
+    def _serve_fused(self, plan: StepPlan, xs: torch.Tensor) -> torch.Tensor:
+        """serve() with the fused exchange: the O / down projections write
+        into the IPC-shared buffers, fs_ar_residual adds the ordered sum."""
+        T = plan.T
+        for layer in range(self.model.num_layers):
+            ia, im = (0, 1) if self.mlp else (layer & 1, None)
+            self._attention(layer, plan)
+            torch.matmul(self.o_s[:T], self.wo[layer], out=self.xchg.partial(ia, xs.shape))
+            self.xchg.reduce_residual(ia, xs)
+            if self.mlp:
+                part = self.xchg.partial(im, xs.shape)
+                if len(self.ffn_cols):
+                    C = len(self.ffn_cols)
+                    torch.matmul(xs, self.w_gu[layer], out=self.h_s[:T])
+                    N.check(N.lib.fs_swiglu(N.ptr(self.h_s), T, C, 2 * C, N.ptr(self.act_s), C,
+                                            _stream()), "fs_swiglu")
+                    torch.matmul(self.act_s[:T], self.w_d[layer], out=part)
+                else:
+                    part.zero_()
+                self.xchg.reduce_residual(im, xs)
         return xs
 
     def serve_launches(self, plan: StepPlan) -> int:

@@ -130,3 +130,47 @@ def test_fused_exchange_decode_step_matches_emulation():
     for rank, ok, ok2, err in _run(_step_worker, 2):
         assert err is None, err
         assert ok and ok2, (rank, ok, ok2)
+
+
+def _serve_worker(rank, world, port, q):
+    try:
+        dist = _init(rank, world, port)
+        from paper_2511_14116_b200.core import ModelSpec
+        from paper_2511_14116_b200.placement import make_placement, owner_array
+        from paper_2511_14116_b200.serving import (HybridServingRank, StepBatch,
+                                                   emulated_serving_step)
+        model = ModelSpec(num_layers=2, num_kv_heads=8, num_q_heads=64, head_dim=128,
+                          hidden_dim=512, ffn_intermediate_dim=1024, ffn_num_shards=16)
+        plan = make_placement("hybrid", model, range(world))
+        owner = owner_array(plan, 8)
+        shards = [plan.ffn.owner[s] for s in range(plan.ffn.num_shards)]
+        caps = [80, 40, 120]
+        routing = {r: r % world for r in range(3)}
+        batch = StepBatch(prefill=[(0, 0, 30), (2, 64, 40)], decode=[(1, 20)])
+
+        def engine(g, group, exchange):
+            e = HybridServingRank(model, owner, g, routing, caps, 96, seed=3, group=group,
+                                  shard_owner=shards, exchange=exchange)
+            e.fill_random_kv(5 + g)
+            return e
+        x = torch.randn((batch.num_tokens, 512), generator=torch.Generator().manual_seed(9))
+        x = x.to(torch.bfloat16).cuda()
+        mine = engine(rank, dist.group.WORLD, "fused")
+        y = mine.serve(mine.plan(batch), x).clone()
+        emu = [engine(g, None, "nccl") for g in range(world)]
+        ref = emulated_serving_step(emu, [e.plan(batch) for e in emu], x)
+        ok = torch.equal(y, ref)
+        mine.xchg.close()
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, ok, True, None))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, False, False, repr(e)))
+
+
+def test_fused_exchange_serving_iteration_matches_emulation():
+    """A mixed prefill/decode iteration (K8 + K1) on 2 real ranks with the
+    fused exchange == the single-process emulation, bit for bit."""
+    for rank, ok, _, err in _run(_serve_worker, 2):
+        assert err is None, err
+        assert ok, rank
