@@ -590,6 +590,7 @@ def run_ours(args, world, rank, local_rank):
     traffic, _ = ncu_traffic() if world == 1 else (None, None)  # capture is of the N=1 config
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
+                "frac_of_nominal_8tbs": round(achieved / 8000.0, 4),
                 "kernel": "decode_kernel (fs_decode_attention: fused KV append + paged GQA "
                           "decode + in-kernel split merge), one launch per layer",
                 "bytes_per_launch": int(per_launch_bytes),
