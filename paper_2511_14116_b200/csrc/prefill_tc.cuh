@@ -83,6 +83,14 @@ __device__ __forceinline__ void tc_commit_bar(uint32_t bar) {
                  : "memory");
 }
 
+// one lane of the (converged) warp: true on exactly one lane
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+                 : "=r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -174,13 +182,18 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
     if (warp == kSoftWarps) {
         // ---------------- TMA producer ----------------
         const int64_t row = (int64_t)p.item_seq[item] * p.bt_stride + pg0;
-        int64_t ids = 0;
+        // page ids 32 at a time (lane = page), the next 32 prefetched a
+        // chunk ahead so the block-table load latency stays off the ring
+        int64_t ids = lane < npg ? p.bt[row + lane] : 0;
+        int64_t ids_next = 32 + lane < npg ? p.bt[row + 32 + lane] : 0;
         for (int j = 0; j < nb; ++j) {
             const int st = j % kTcStages;
-            if (j >= kTcStages) {
-                if (lane == 0) mbar_wait(kv_empty + 8 * st, ((j / kTcStages) - 1) & 1);
-                __syncwarp();
+            if (j > 0 && (j & 7) == 0) {
+                ids = ids_next;
+                const int k = 4 * j + 32 + lane;
+                ids_next = k < npg ? p.bt[row + k] : 0;
             }
+            if (j >= kTcStages) mbar_wait(kv_empty + 8 * st, ((j / kTcStages) - 1) & 1);
             const int np = min(4, npg - 4 * j);
             const uint32_t ks = kv_s + 2 * st * kTcKVBytes, vs = ks + kTcKVBytes;
             if (np < 4) {
@@ -192,41 +205,39 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
                         make_uint4(0, 0, 0, 0);
                 }
                 fence_proxy_async();
-                __syncwarp();
             }
-            for (int pp = 0; pp < np; ++pp) {
-                const int k = 4 * j + pp;
-                if ((k & 31) == 0) ids = k + lane < npg ? p.bt[row + k + lane] : 0;
-                const int64_t pg = __shfl_sync(0xffffffffu, ids, k & 31);
-                if (lane == 0) {
-                    if (pp == 0) mbar_expect_tx(kv_full + 8 * st, np * kPageBytes);
-                    const uint8_t *src = p.kv + pg * kPageBytes;
-                    for (int a = 0; a < 2; ++a) {
-                        bulk_g2s_plain(ks + a * 8192 + pp * 2048, src + a * kAtomBytes, kAtomBytes,
-                                       kv_full + 8 * st);
-                        bulk_g2s_plain(vs + a * 8192 + pp * 2048, src + kHalfPage + a * kAtomBytes,
-                                       kAtomBytes, kv_full + 8 * st);
-                    }
-                }
-            }
+            if (lane == 0) mbar_expect_tx(kv_full + 8 * st, np * kPageBytes);
+            __syncwarp();
+            // lane l < 4 * np copies one 2 KB atom: page l >> 2, K/V (l & 1),
+            // atom (l >> 1) & 1
+            const int pp = lane >> 2, half = lane & 1, a = (lane >> 1) & 1;
+            const int64_t pg = __shfl_sync(0xffffffffu, ids, (4 * j + pp) & 31);
+            if (lane < 4 * np)
+                bulk_g2s_plain((half ? vs : ks) + a * 8192 + pp * 2048,
+                               p.kv + pg * kPageBytes + half * kHalfPage + a * kAtomBytes, kAtomBytes,
+                               kv_full + 8 * st);
         }
     } else if (warp == kSoftWarps + 1) {
         // ---------------- MMA issuer ----------------
-        if (lane == 0) {
-            mbar_wait(q_ready, 0);
-            tc_after();
-            auto issue_s = [&](int j) {
-                const int st = j % kTcStages, b = j & 1;
-                mbar_wait(kv_full + 8 * st, (j / kTcStages) & 1);
-                const uint32_t ks = kv_s + 2 * st * kTcKVBytes;
+        // The whole warp runs the loop so descriptors and TMEM addresses are
+        // warp-uniform (uniform datapath, no per-MMA R2UR waterfall); one
+        // elected lane issues.  Issuing from lane 0 alone measured ~1.4x
+        // slower than the tensor pipe (tools/ubench/mma_rate.cu, twohalf).
+        mbar_wait(q_ready, 0);
+        tc_after();
+        auto issue_s = [&](int j) {
+            const int st = j % kTcStages, b = j & 1;
+            mbar_wait(kv_full + 8 * st, (j / kTcStages) & 1);
+            const uint32_t ks = kv_s + 2 * st * kTcKVBytes;
 #pragma unroll
-                for (int h = 0; h < NQ; ++h) {
-                    // S_j overwrites the TMEM columns P_{j-2} occupied: the
-                    // tensor pipe runs this thread's MMAs in issue order, so
-                    // P.V_{j-2} (issued earlier) has read them
-                    tc_after();
-                    const uint32_t qh = q_s + h * kTcQBytes;
-                    const uint32_t s_t = tmem + 256 * h + kHeadDim + b * kTcKeys;
+            for (int h = 0; h < NQ; ++h) {
+                // S_j overwrites the TMEM columns P_{j-2} occupied: the
+                // tensor pipe runs this warp's MMAs in issue order, so
+                // P.V_{j-2} (issued earlier) has read them
+                tc_after();
+                const uint32_t qh = q_s + h * kTcQBytes;
+                const uint32_t s_t = tmem + 256 * h + kHeadDim + b * kTcKeys;
+                if (elect_one()) {
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
                         const uint64_t ad = tc_desc(qh + (k >> 2) * (kTcRows * 128) + (k & 3) * 32, 16, 1024);
@@ -235,17 +246,20 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
                     }
                     tc_commit_bar(s_full + 8 * (2 * h + b));
                 }
-            };
-            issue_s(0);
-            if (nb > 1) issue_s(1);
-            for (int j = 0; j < nb; ++j) {
-                const int st = j % kTcStages, b = j & 1;
-                const uint32_t vs = kv_s + (2 * st + 1) * kTcKVBytes;
+                __syncwarp();
+            }
+        };
+        issue_s(0);
+        if (nb > 1) issue_s(1);
+        for (int j = 0; j < nb; ++j) {
+            const int st = j % kTcStages, b = j & 1;
+            const uint32_t vs = kv_s + (2 * st + 1) * kTcKVBytes;
 #pragma unroll
-                for (int h = 0; h < NQ; ++h) {
-                    mbar_wait(p_full + 8 * (2 * h + b), (j >> 1) & 1);
-                    tc_after();
-                    const uint32_t pt = tmem + 256 * h + kHeadDim + b * kTcKeys;  // P over S_j
+            for (int h = 0; h < NQ; ++h) {
+                mbar_wait(p_full + 8 * (2 * h + b), (j >> 1) & 1);
+                tc_after();
+                const uint32_t pt = tmem + 256 * h + kHeadDim + b * kTcKeys;  // P over S_j
+                if (elect_one()) {
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         const uint64_t bd = tc_desc(vs + k * 2048, kTcKeys * 128, 1024);
@@ -253,9 +267,11 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
                     }
                     tc_commit_bar(o_done + 8 * (2 * h + b));
                 }
-                tc_commit_bar(kv_empty + 8 * st);
-                if (j + 2 < nb) issue_s(j + 2);
+                __syncwarp();
             }
+            if (elect_one()) tc_commit_bar(kv_empty + 8 * st);
+            __syncwarp();
+            if (j + 2 < nb) issue_s(j + 2);
         }
     } else {
         // ---------------- softmax / correction / epilogue (row = thread) ----------------

@@ -1,0 +1,61 @@
+"""Dev tool: patch a copy of csrc/prefill_tc.cuh with per-CTA globaltimer stamps
+(kernel start, first S issue, MMA loop end, CTA end, SM id, #blocks) written to
+part_lse + 1e6 (tools/tl_dbg2.py reads them) and/or a softmax ablation
+(FS_TC_EXP=1: publish P without computing it).  Never commit the patched file."""
+import sys
+p = "paper_2511_14116_b200/csrc/prefill_tc.cuh"
+s = open(p).read()
+mode = sys.argv[1]
+if "timeline" in mode:
+    s = s.replace('''    const int nb = (npg + 3) >> 2;  // 64-key blocks
+''', '''    const int nb = (npg + 3) >> 2;  // 64-key blocks
+    long long *dbgp = reinterpret_cast<long long *>(p.part_lse) + 1000000 + blockIdx.x * 8;
+    auto gtm = []() { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return (long long)t; };
+    if (threadIdx.x == 0) { unsigned sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm)); dbgp[0] = gtm(); dbgp[4] = sm; dbgp[5] = nb; }
+''', 1)
+    s = s.replace('''        issue_s(0);
+        if (nb > 1) issue_s(1);''', '''        if (lane == 0) dbgp[1] = gtm();
+        issue_s(0);
+        if (nb > 1) issue_s(1);''', 1)
+    s = s.replace('''            if (j + 2 < nb) issue_s(j + 2);
+        }''', '''            if (j + 2 < nb) issue_s(j + 2);
+        }
+        if (lane == 0) dbgp[2] = gtm();''', 1)
+    s = s.replace('''    tc_before();
+    __syncthreads();
+    if (warp == kSoftWarps + 1) {
+        tc_after();
+        asm volatile("tcgen05.dealloc''', '''    tc_before();
+    __syncthreads();
+    if (threadIdx.x == 0) dbgp[3] = gtm();
+    if (warp == kSoftWarps + 1) {
+        tc_after();
+        asm volatile("tcgen05.dealloc''', 1)
+    assert s.count("dbgp") >= 6, "timeline patch failed"
+if "waits" in mode:
+    # cycles the MMA warp spends waiting for K/V (kv_full) and for P (p_full)
+    s = s.replace("""        auto issue_s = [&](int j) {
+            const int st = j % kTcStages, b = j & 1;
+            mbar_wait(kv_full + 8 * st, (j / kTcStages) & 1);""", """        long long w_kv = 0, w_p = 0, c_loop0 = clock64();
+        auto issue_s = [&](int j) {
+            const int st = j % kTcStages, b = j & 1;
+            { long long c0 = clock64(); mbar_wait(kv_full + 8 * st, (j / kTcStages) & 1); w_kv += clock64() - c0; }""", 1)
+    s = s.replace("""                mbar_wait(p_full + 8 * (2 * h + b), (j >> 1) & 1);
+                tc_after();
+                const uint32_t pt""", """                { long long c0 = clock64(); mbar_wait(p_full + 8 * (2 * h + b), (j >> 1) & 1); w_p += clock64() - c0; }
+                tc_after();
+                const uint32_t pt""", 1)
+    s = s.replace("""        if (lane == 0) dbgp[2] = gtm();""", """        if (lane == 0) { dbgp[2] = gtm(); dbgp[6] = w_kv; dbgp[7] = w_p; dbgp[5] |= (clock64() - c_loop0) << 16; }""", 1)
+    assert s.count("w_kv") == 3, s.count("w_kv")
+if "nosoftmax" in mode:
+    old = '''            uint32_t sr[2][32];
+            tc_ld32(s_t + b * kTcKeys, sr[0]);'''
+    assert old in s
+    s = s.replace(old, '''            if (true) {
+                tc_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cta(p_full + 8 * hb);
+                continue;
+            }
+''' + old, 1)
+open(p, "w").write(s)
