@@ -29,6 +29,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <functional>
 #include <numeric>
 #include <vector>
 
@@ -285,56 +286,78 @@ __global__ void __launch_bounds__((kConsumerWarps + 2) * 32) prefill_kernel(cons
 // merge the page-range splits of one (item, token tile); grid.y = 64-row
 // slabs of the tile: 4 threads per row,
 // 32 dims each, log-sum-exp weights in base 2
+// One CTA = 16 rows x 16 threads of one combine group; a thread owns 8 dims
+// of its row (a warp reads two contiguous 512-B partial rows per load).  The
+// split loop keeps 4 splits' loads in flight (the merge is latency-bound, not
+// bandwidth-bound, at the few-hundred-KB-per-SM sizes K8 produces).  Launched
+// with PDL: it is scheduled during the attention kernel's tail and waits in
+// griddepcontrol.wait for its partials.
+constexpr int kCombRows = 16;
+
 __global__ void __launch_bounds__(256) prefill_combine_kernel(const PrefillParams p) {
+    grid_dependency_wait();
     const int g = blockIdx.x;
     const int item = p.comb_item[g], tok0 = p.comb_tok0[g];
     const int slot0 = p.comb_slot0[g], ns = p.comb_nsplit[g];
-    const int r = blockIdx.y * 64 + (threadIdx.x >> 2), part = threadIdx.x & 3;  // 64-row slabs
+    const int r = blockIdx.y * kCombRows + (threadIdx.x >> 4), c = threadIdx.x & 15;
     const int qpk = p.qpk, rows_used = p.tpt * qpk;
     if (r >= rows_used) return;
     const int tok = tok0 + r / qpk, h = r % qpk;
     if (tok >= p.item_len[item]) return;
+    const float *lse = p.part_lse + (int64_t)slot0 * p.rows + r;
     float mx = -INFINITY;
-    for (int s = 0; s < ns; ++s) mx = fmaxf(mx, p.part_lse[(int64_t)(slot0 + s) * p.rows + r]);
-    float acc[32];
+    for (int s0 = 0; s0 < ns; s0 += 8) {
+        float v[8];
 #pragma unroll
-    for (int d = 0; d < 32; ++d) acc[d] = 0.f;
+        for (int i = 0; i < 8; ++i) v[i] = s0 + i < ns ? __ldg(lse + (int64_t)(s0 + i) * p.rows) : -INFINITY;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx = fmaxf(mx, v[i]);
+    }
+    const float4 *po = reinterpret_cast<const float4 *>(p.part_o + ((int64_t)slot0 * p.rows + r) * kHeadDim) + 2 * c;
+    const int64_t sstr = (int64_t)p.rows * (kHeadDim / 4);  // float4s per split slot
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     float den = 0.f;
-    for (int s = 0; s < ns; ++s) {
-        const float lse = p.part_lse[(int64_t)(slot0 + s) * p.rows + r];
-        const float w = lse == -INFINITY ? 0.f : fast_exp2(lse - mx);
-        den += w;
-        const float4 *src = reinterpret_cast<const float4 *>(
-            p.part_o + ((int64_t)(slot0 + s) * p.rows + r) * kHeadDim + part * 32);
+    for (int s0 = 0; s0 < ns; s0 += 4) {
+        float w[4];
+        float4 va[4], vb[4];
 #pragma unroll
-        for (int d = 0; d < 8; ++d) {
-            const float4 v = src[d];
-            acc[4 * d] += w * v.x;
-            acc[4 * d + 1] += w * v.y;
-            acc[4 * d + 2] += w * v.z;
-            acc[4 * d + 3] += w * v.w;
+        for (int i = 0; i < 4; ++i) {
+            w[i] = 0.f;
+            va[i] = vb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (s0 + i < ns) {
+                const float l = __ldg(lse + (int64_t)(s0 + i) * p.rows);
+                w[i] = l == -INFINITY ? 0.f : fast_exp2(l - mx);
+                va[i] = __ldg(po + (s0 + i) * sstr);
+                vb[i] = __ldg(po + (s0 + i) * sstr + 1);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            den += w[i];
+            acc[0] += w[i] * va[i].x;
+            acc[1] += w[i] * va[i].y;
+            acc[2] += w[i] * va[i].z;
+            acc[3] += w[i] * va[i].w;
+            acc[4] += w[i] * vb[i].x;
+            acc[5] += w[i] * vb[i].y;
+            acc[6] += w[i] * vb[i].z;
+            acc[7] += w[i] * vb[i].w;
         }
     }
     const float inv = den > 0.f ? 1.f / den : 0.f;
-    const int64_t o = p.item_ooff[item] + (int64_t)tok * p.o_stride + h * kHeadDim + part * 32;
+    const int64_t o = p.item_ooff[item] + (int64_t)tok * p.o_stride + h * kHeadDim + c * 8;
     if (p.out_fp32) {
         float4 *dst = reinterpret_cast<float4 *>(static_cast<float *>(p.out) + o);
-#pragma unroll
-        for (int d = 0; d < 8; ++d)
-            dst[d] = make_float4(acc[4 * d] * inv, acc[4 * d + 1] * inv, acc[4 * d + 2] * inv,
-                                 acc[4 * d + 3] * inv);
+        dst[0] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+        dst[1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
         return;
     }
-    __nv_bfloat16 *dst = static_cast<__nv_bfloat16 *>(p.out) + o;
-#pragma unroll
-    for (int d = 0; d < 32; d += 8) {
-        uint4 pk;
-        pk.x = pack_bf16(acc[d] * inv, acc[d + 1] * inv);
-        pk.y = pack_bf16(acc[d + 2] * inv, acc[d + 3] * inv);
-        pk.z = pack_bf16(acc[d + 4] * inv, acc[d + 5] * inv);
-        pk.w = pack_bf16(acc[d + 6] * inv, acc[d + 7] * inv);
-        *reinterpret_cast<uint4 *>(dst + d) = pk;
-    }
+    uint4 pk;
+    pk.x = pack_bf16(acc[0] * inv, acc[1] * inv);
+    pk.y = pack_bf16(acc[2] * inv, acc[3] * inv);
+    pk.z = pack_bf16(acc[4] * inv, acc[5] * inv);
+    pk.w = pack_bf16(acc[6] * inv, acc[7] * inv);
+    *reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.out) + o) = pk;
 }
 
 #include "prefill_tc.cuh"
@@ -380,18 +403,43 @@ extern "C" int fs_plan_prefill_tiles(int32_t n_items, const int32_t *item_start,
             work += pages;
         }
     }
-    // pages per split: at least 32 (a split below that is all pipeline
-    // fill); grown until the tile count fits in target_units, so a launch of
-    // similar tiles is whole waves (a partial last wave of equal-size tiles
-    // idles the other SMs for a full tile time)
+    // Pages per split: at least 32 (a split below that is all pipeline
+    // fill).  target_units is the number of CTAs that run at once (one
+    // tcgen05 CTA per SM); the split size is the one whose tiles, dispatched
+    // heaviest first onto target_units slots (what the block scheduler does
+    // with the sorted tile list), finish earliest -- each tile costing its
+    // pages plus kTileOverheadPages for its prologue / epilogue / combine
+    // share (measured: ~8 us per tile vs ~0.28 us per page on B200).
+    constexpr int64_t kTileOverheadPages = 28;
     const int64_t units = std::max<int64_t>(1, target_units);
-    int32_t per = (int32_t)std::max<int64_t>(32, (work + units - 1) / units);
-    auto count = [&](int32_t q) {
-        int64_t n = 0;
-        for (const Tok &tk : toks) n += (tk.pages + q - 1) / q;
-        return n;
+    int32_t max_pages = 1;
+    for (const Tok &tk : toks) max_pages = std::max(max_pages, tk.pages);
+    std::vector<int64_t> sizes, load;
+    auto makespan = [&](int32_t q) {
+        sizes.clear();
+        for (const Tok &tk : toks) {
+            const int ns = (tk.pages + q - 1) / q;
+            for (int s = 0; s < ns; ++s)
+                sizes.push_back((int64_t)tk.pages * (s + 1) / ns - (int64_t)tk.pages * s / ns);
+        }
+        std::sort(sizes.begin(), sizes.end(), std::greater<int64_t>());
+        load.assign((size_t)std::min<int64_t>(units, (int64_t)sizes.size()), 0);
+        std::make_heap(load.begin(), load.end(), std::greater<int64_t>());
+        int64_t worst = 0;
+        for (int64_t w : sizes) {  // least-loaded slot takes the next tile
+            std::pop_heap(load.begin(), load.end(), std::greater<int64_t>());
+            load.back() += w + kTileOverheadPages;
+            worst = std::max(worst, load.back());
+            std::push_heap(load.begin(), load.end(), std::greater<int64_t>());
+        }
+        return worst;
     };
-    while ((int64_t)toks.size() < units && count(per) > units) per += std::max(1, per / 16);
+    int32_t per = std::max<int32_t>(32, max_pages);
+    int64_t best = makespan(per);
+    for (int32_t q = 32; q < max_pages; q += std::max(1, q / 12)) {
+        const int64_t m = makespan(q);
+        if (m < best) best = m, per = q;
+    }
     struct Tile { int32_t item, tok0, p0, p1, slot; };
     std::vector<Tile> tiles;
     int32_t slots = 0, nc = 0;
@@ -508,7 +556,16 @@ extern "C" int fs_prefill_attention(const fs_prefill_desc *d, void *stream) {
     }
     FS_CUDA(cudaGetLastError());
     if (d->n_comb > 0) {
-        prefill_combine_kernel<<<dim3(d->n_comb, prm.rows / 64), 256, 0, st>>>(prm);
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(d->n_comb, prm.rows / kCombRows);
+        lc.blockDim = dim3(256);
+        lc.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = attr;
+        lc.numAttrs = 1;
+        FS_CUDA(cudaLaunchKernelEx(&lc, prefill_combine_kernel, prm));
         FS_CUDA(cudaGetLastError());
     }
     return FS_OK;

@@ -291,14 +291,25 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
         const float scale = p.scale_log2;
         // ---- Q row -> smem (2 SW128 atoms of this half) ----
         {
-            const uint4 *src = reinterpret_cast<const uint4 *>(p.q + p.item_qoff[item] +
-                                                               (int64_t)tok * p.q_stride + hd * kHeadDim);
+            // the warp loads its 32 rows cooperatively, two 256-B rows per
+            // instruction (rows of one token are adjacent heads: coalesced),
+            // all 16 loads in flight before the swizzled smem stores
+            const __nv_bfloat16 *qb = p.q + p.item_qoff[item];
+            const int c = lane & 15;
+            uint4 v[16];
 #pragma unroll
-            for (int c = 0; c < 16; ++c) {
-                const uint4 v = src[c];
-                const uint32_t off = h * kTcQBytes + (c >> 3) * (kTcRows * 128) + r * 128 +
-                                     (((c & 7) ^ (r & 7)) << 4);
-                *reinterpret_cast<uint4 *>(smem + (q_s - sb) + off) = v;
+            for (int i = 0; i < 16; ++i) {
+                const int Ri = h * kTcRows + (warp & 3) * 32 + 2 * i + (lane >> 4);
+                const int tki = min(tok0 + min(Ri, rows_used - 1) / qpk, n - 1);
+                v[i] = __ldg(reinterpret_cast<const uint4 *>(qb + (int64_t)tki * p.q_stride +
+                                                             (Ri % qpk) * kHeadDim) + c);
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int ri = (warp & 3) * 32 + 2 * i + (lane >> 4);  // row within the half
+                const uint32_t off = h * kTcQBytes + (c >> 3) * (kTcRows * 128) + ri * 128 +
+                                     (((c & 7) ^ (ri & 7)) << 4);
+                *reinterpret_cast<uint4 *>(smem + (q_s - sb) + off) = v[i];
             }
             fence_proxy_async();
             __syncwarp();
@@ -379,6 +390,7 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
             if (lane == 0) mbar_arrive_cta(p_full + 8 * hb);
         }
         // ---- epilogue: O / l (or the split partial) ----
+        grid_launch_dependents();  // the combine launch (PDL) may be scheduled now
         mbar_wait(o_done + 8 * (2 * h + ((nb - 1) & 1)), ((nb - 1) >> 1) & 1);
         tc_after();
         const float inv = l > 0.f ? 1.f / l : 0.f;

@@ -28,9 +28,9 @@ DEFAULT_VARIANT = 0
 
 
 def default_target_units(device_index: int, variant: int = DEFAULT_VARIANT) -> int:
-    """Tiles the planner aims for: 2 per SM for the tcgen05 variants (one
-    ~225-KB CTA per SM), 4 per SM for the mma.sync variant."""
-    return (4 if variant == 1 else 2) * N.lib.fs_device_sms(device_index)
+    """CTAs that run at once, the planner's parallel slots: one ~225-KB
+    tcgen05 CTA per SM, 4 per SM for the mma.sync variant."""
+    return (4 if variant == 1 else 1) * N.lib.fs_device_sms(device_index)
 
 
 def _stream():

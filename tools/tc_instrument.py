@@ -47,6 +47,30 @@ if "waits" in mode:
                 const uint32_t pt""", 1)
     s = s.replace("""        if (lane == 0) dbgp[2] = gtm();""", """        if (lane == 0) { dbgp[2] = gtm(); dbgp[6] = w_kv; dbgp[7] = w_p; dbgp[5] |= (clock64() - c_loop0) << 16; }""", 1)
     assert s.count("w_kv") == 3, s.count("w_kv")
+if "prologue" in mode:
+    # dbg[6] = after setup barrier (thread 0), dbg[7] = softmax warp 0 Q rows stored
+    s = s.replace("""    const uint32_t tmem = *tmem_slot;
+""", """    const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) dbgp[6] = gtm();
+""", 1)
+    s = s.replace("""            if (lane == 0) mbar_arrive_cta(q_ready);""", """            if (lane == 0) mbar_arrive_cta(q_ready);
+            if (threadIdx.x == 0) dbgp[7] = gtm();""", 1)
+if "qload" in mode:
+    # dbg[1] (reused) = params loaded, dbg[2] = Q loads returned, dbg[7] = Q stored (thread 0)
+    s = s.replace("""            uint4 v[16];""", """            if (threadIdx.x == 0) { dbgp[1] = gtm() + 0 * (start + n + (long long)qb); }
+            uint4 v[16];""", 1)
+    s = s.replace("""#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int ri = (warp & 3) * 32""", """            if (threadIdx.x == 0) { uint32_t x = 0; for (int i = 0; i < 16; ++i) x ^= v[i].x; dbgp[2] = gtm() + (x == 0x12345 ? 1 : 0); }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int ri = (warp & 3) * 32""", 1)
+    s = s.replace("""            if (lane == 0) mbar_arrive_cta(q_ready);""", """            if (lane == 0) mbar_arrive_cta(q_ready);
+            if (threadIdx.x == 0) dbgp[7] = gtm();""", 1)
+    s = s.replace("""    const uint32_t tmem = *tmem_slot;
+""", """    const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) dbgp[6] = gtm();
+""", 1)
 if "nosoftmax" in mode:
     old = '''            uint32_t sr[2][32];
             tc_ld32(s_t + b * kTcKeys, sr[0]);'''

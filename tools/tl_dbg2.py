@@ -20,12 +20,15 @@ s.record(); L(q, stride, out, stride); e.record(); torch.cuda.synchronize()
 print("launch ms", s.elapsed_time(e))
 n = L.n_tiles
 d = L.part_lse.view(torch.int64)[1000000:1000000 + n * 8].view(n, 8).cpu().numpy()
+np.save("gpurun_out/qload.npy", d)
 t0 = d[:, 0].min()
 st_, mma0, mma1, end, sm, nb = [d[:, i] for i in range(6)]
 cyc = nb >> 16; nb = nb & 0xffff
 if cyc.any():
     print("MMA warp per block: loop cycles %.0f, kv_full wait %.0f, p_full wait %.0f" % (
         np.median(cyc / nb), np.median(d[:, 6] / nb), np.median(d[:, 7] / nb)))
+if not cyc.any() and d[:, 6].any():
+    print("setup us %.2f, Q stored us %.2f (from CTA start)" % (np.median(d[:, 6] - st_) / 1e3, np.median(d[:, 7] - st_) / 1e3))
 print("tiles", n, "kernel span us", (end.max() - t0) / 1e3)
 print("start spread us", (st_.max() - t0) / 1e3)
 pro = (mma0 - st_) / 1e3; loop = (mma1 - mma0) / 1e3; epi = (end - mma1) / 1e3
