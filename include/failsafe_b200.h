@@ -197,12 +197,14 @@ typedef struct fs_prefill_desc {
     float *part_lse;           /* [partial_slots][rows]                     */
     int64_t partial_slots;
     int32_t variant;           /* 0: tcgen05 (TMEM accumulators, 256-row
-                                  tiles = two 128-row halves); 1: mma.sync
-                                  (64-row tiles); 2: tcgen05, 128 rows     */
+                                  tiles = two 128-row halves, 64-key
+                                  blocks); 1: mma.sync (64-row tiles);
+                                  2: tcgen05, 128 rows; 3: as 0 with
+                                  128-key blocks                           */
 } fs_prefill_desc;
 
-/* chunk tokens per tile (rows / q_per_kv; rows = 256 / 64 / 128 for
- * variants 0 / 1 / 2), or <0 */
+/* chunk tokens per tile (rows / q_per_kv; rows = 256 / 64 / 128 / 256 for
+ * variants 0 / 1 / 2 / 3), or <0 */
 int fs_prefill_tokens_per_tile(int q_per_kv, int variant);
 
 /* Host planner of the K8 launch: token tiles of every item, each split into

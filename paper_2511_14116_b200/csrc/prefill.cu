@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(256) prefill_combine_kernel(const PrefillParam
 // query rows per tile of each kernel variant (0: tcgen05 with two 128-row
 // halves, 1: mma.sync, 2: tcgen05 with one 128-row half)
 static int variant_rows(int variant) {
-    return variant == 0 ? 2 * kTcRows : variant == 1 ? kTileRows : variant == 2 ? kTcRows : -1;
+    return variant == 0 || variant == 3 ? 2 * kTcRows : variant == 1 ? kTileRows : variant == 2 ? kTcRows : -1;
 }
 
 }  // namespace fs
@@ -526,24 +526,21 @@ extern "C" int fs_prefill_attention(const fs_prefill_desc *d, void *stream) {
     prm.part_o = d->part_o;
     prm.part_lse = d->part_lse;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    static bool attr_set[3][64] = {{false}};
+    static bool attr_set[4][64] = {{false}};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (d->variant == 0 || d->variant == 2) {
-        const int v = d->variant == 0 ? 0 : 2;
-        if (!attr_set[v == 0 ? 0 : 2][dev & 63]) {
-            if (v == 0)
-                FS_CUDA(cudaFuncSetAttribute(prefill_tc_kernel<2>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem<2>()));
-            else
-                FS_CUDA(cudaFuncSetAttribute(prefill_tc_kernel<1>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem<1>()));
-            attr_set[v == 0 ? 0 : 2][dev & 63] = true;
+    if (d->variant == 0 || d->variant == 2 || d->variant == 3) {
+        // tcgen05: 0 = two 128-row halves x 64-key blocks, 2 = one half,
+        // 3 = two halves x 128-key blocks
+        const int v = d->variant;
+        auto kfn = v == 0 ? prefill_tc_kernel<2, 64> : v == 2 ? prefill_tc_kernel<1, 64> : prefill_tc_kernel<2, 128>;
+        const int smem = v == 0 ? tc_smem<2, 64>() : v == 2 ? tc_smem<1, 64>() : tc_smem<2, 128>();
+        const int threads = (v == 2 ? 1 : 2) * 128 + 64;
+        if (!attr_set[v][dev & 63]) {
+            FS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            attr_set[v][dev & 63] = true;
         }
-        if (v == 0)
-            prefill_tc_kernel<2><<<d->n_tiles, 2 * 128 + 64, tc_smem<2>(), st>>>(prm);
-        else
-            prefill_tc_kernel<1><<<d->n_tiles, 128 + 64, tc_smem<1>(), st>>>(prm);
+        kfn<<<d->n_tiles, threads, smem, st>>>(prm);
     } else {
         constexpr int S = kPrefillStages;
         const size_t smem = (size_t)S * kPageBytes + 3 * S * 8;

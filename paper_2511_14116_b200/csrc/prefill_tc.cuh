@@ -27,21 +27,27 @@
 // [192, 256).
 
 constexpr int kTcRows = 128;                      // rows per Q half-tile (UMMA M)
-constexpr int kTcKeys = 64;                       // keys per block (4 pages)
-constexpr int kTcStages = 5;                      // K/V block ring
 constexpr int kTcQBytes = kTcRows * 256;          // 32 KB: 2 atoms x 128 rows x 128 B
-constexpr int kTcKVBytes = kTcKeys * 256;         // 16 KB: 2 atoms x 64 rows x 128 B
-template <int NQ>
+// keys per block BK = 64 (4 pages) or 128 (8 pages); per BK: K/V ring depth
+// and S buffers per half (TMEM: O 128 columns + kTcSBuf x BK per half)
+// separate K and V rings: K_j is released once S_j ran, V_j once P.V_j ran,
+// so K can run further ahead (S_{j+1} is issued before P.V_j's inputs are free)
+template <int BK> constexpr int tc_kstages() { return BK == 64 ? 5 : 3; }
+template <int BK> constexpr int tc_vstages() { return BK == 64 ? 5 : 2; }
+template <int BK> constexpr int tc_sbuf() { return BK == 64 ? 2 : 1; }
+template <int NQ, int BK>
 constexpr int tc_smem() {
-    return NQ * kTcQBytes + 2 * kTcStages * kTcKVBytes + 1024 + 512;
+    return NQ * kTcQBytes + (tc_kstages<BK>() + tc_vstages<BK>()) * (BK * 256) + 1024 + 512;
 }
 constexpr float kTcRescale = 8.f;                 // lazy-rescale threshold (log2)
 
 // kind::f16 instruction descriptors: D fp32; S: A = Q bf16 K-major, B = K
 // bf16 K-major, M 128, N 64; PV: A = P f16 K-major, B = V f16 MN-major,
 // M 128, N 128
-constexpr uint32_t kIdescS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTcKeys >> 3) << 17) |
-                             ((uint32_t)(kTcRows >> 4) << 24);
+template <int BK>
+constexpr uint32_t tc_idesc_s() {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BK >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
+}
 constexpr uint32_t kIdescPV = (1u << 4) | (1u << 16) | ((uint32_t)(kHeadDim >> 3) << 17) |
                               ((uint32_t)(kTcRows >> 4) << 24);
 
@@ -91,6 +97,32 @@ __device__ __forceinline__ bool elect_one() {
     return pred != 0;
 }
 
+// packed fp32x2 arithmetic (FFMA2 / FADD2) and the 3-input max (FMNMX3) of
+// sm_100: half the softmax's FMA-pipe instructions per element
+__device__ __forceinline__ uint64_t f2(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void f2_split(uint64_t v, float &a, float &b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
 __device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -119,6 +151,15 @@ __device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t (&r)[32])
         : "memory");
 }
 
+__device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -131,8 +172,13 @@ __device__ __forceinline__ void bulk_g2s_plain(uint32_t dst, const void *src, ui
         : "memory");
 }
 
-template <int NQ>
+template <int NQ, int BK>
 __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const PrefillParams p) {
+    constexpr int kTcKeys = BK, kPB = BK / 16;        // keys / pages per block
+    constexpr int kKS = tc_kstages<BK>(), kVS = tc_vstages<BK>(), kSBuf = tc_sbuf<BK>();
+    constexpr int kTcKVBytes = BK * 256;              // K or V of a block: 2 atoms x BK rows x 128 B
+    constexpr int kAtom = BK * 128;                   // one 64-dim atom of a block
+    constexpr uint32_t kIdescS = tc_idesc_s<BK>();
     constexpr int kSoftWarps = 4 * NQ;
     constexpr int kTmemCols = 256 * NQ;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -140,11 +186,13 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sb = smem_u32(smem);
     const uint32_t q_s = sb;                                       // half h at + h*32K
-    const uint32_t kv_s = q_s + NQ * kTcQBytes;                    // stage s: K at +2s*16K, V at +(2s+1)*16K
-    const uint32_t bars = kv_s + 2 * kTcStages * kTcKVBytes;
-    const uint32_t kv_full = bars, kv_empty = bars + 8 * kTcStages;
+    const uint32_t k_s = q_s + NQ * kTcQBytes;                     // K stage s at + s * kTcKVBytes
+    const uint32_t v_s = k_s + kKS * kTcKVBytes;                   // V stage s at + s * kTcKVBytes
+    const uint32_t bars = v_s + kVS * kTcKVBytes;
+    const uint32_t k_full = bars, k_empty = k_full + 8 * kKS;
+    const uint32_t v_full = k_empty + 8 * kKS, v_empty = v_full + 8 * kVS;
     // per half h and buffer b: barrier + 8 * (2h + b)
-    const uint32_t s_full = bars + 16 * kTcStages;
+    const uint32_t s_full = v_empty + 8 * kVS;
     const uint32_t p_full = s_full + 16 * NQ, o_done = p_full + 16 * NQ, q_ready = o_done + 16 * NQ;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + (q_ready + 8 - sb));
 
@@ -154,12 +202,16 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
     const int tok0 = p.tile_tok0[t];
     const int pg0 = p.tile_page0[t];
     const int npg = p.tile_page1[t] - pg0;
-    const int nb = (npg + 3) >> 2;  // 64-key blocks
+    const int nb = (npg + kPB - 1) / kPB;  // key blocks
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kTcStages; ++s) {
-            mbar_init(kv_full + 8 * s, 1);
-            mbar_init(kv_empty + 8 * s, 1);
+        for (int s = 0; s < kKS; ++s) {
+            mbar_init(k_full + 8 * s, 1);
+            mbar_init(k_empty + 8 * s, 1);
+        }
+        for (int s = 0; s < kVS; ++s) {
+            mbar_init(v_full + 8 * s, 1);
+            mbar_init(v_empty + 8 * s, 1);
         }
         for (int b = 0; b < 2 * NQ; ++b) {
             mbar_init(s_full + 8 * b, 1);
@@ -187,35 +239,45 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
         int64_t ids = lane < npg ? p.bt[row + lane] : 0;
         int64_t ids_next = 32 + lane < npg ? p.bt[row + 32 + lane] : 0;
         for (int j = 0; j < nb; ++j) {
-            const int st = j % kTcStages;
-            if (j > 0 && (j & 7) == 0) {
+            if (j > 0 && (j % (32 / kPB)) == 0) {
                 ids = ids_next;
-                const int k = 4 * j + 32 + lane;
+                const int k = kPB * j + 32 + lane;
                 ids_next = k < npg ? p.bt[row + k] : 0;
             }
-            if (j >= kTcStages) mbar_wait(kv_empty + 8 * st, ((j / kTcStages) - 1) & 1);
-            const int np = min(4, npg - 4 * j);
-            const uint32_t ks = kv_s + 2 * st * kTcKVBytes, vs = ks + kTcKVBytes;
-            if (np < 4) {
-                // keys of missing pages are masked; their V rows must be finite
-                const int per_atom = (4 - np) * 128;  // 16-byte chunks past page np-1
-                for (int c = lane; c < 2 * per_atom; c += 32) {
-                    const int a = c / per_atom, w = c - a * per_atom;
-                    reinterpret_cast<uint4 *>(smem + (vs - sb) + a * 8192 + np * 2048)[w] =
-                        make_uint4(0, 0, 0, 0);
-                }
-                fence_proxy_async();
+            const int np = min(kPB, npg - kPB * j);
+            // lane l < 2 * np copies one 2 KB atom of K (then of V): page
+            // l >> 1, atom l & 1
+            const int pp = lane >> 1, a = lane & 1;
+            const int64_t pg = __shfl_sync(0xffffffffu, ids, (kPB * j + pp) & 31);
+            const uint8_t *src = p.kv + pg * kPageBytes + a * kAtomBytes;
+            {
+                const int st = j % kKS;
+                if (j >= kKS) mbar_wait(k_empty + 8 * st, ((j / kKS) - 1) & 1);
+                if (lane == 0) mbar_expect_tx(k_full + 8 * st, np * kHalfPage);
+                __syncwarp();
+                if (lane < 2 * np)
+                    bulk_g2s_plain(k_s + st * kTcKVBytes + a * kAtom + pp * 2048, src, kAtomBytes,
+                                   k_full + 8 * st);
             }
-            if (lane == 0) mbar_expect_tx(kv_full + 8 * st, np * kPageBytes);
-            __syncwarp();
-            // lane l < 4 * np copies one 2 KB atom: page l >> 2, K/V (l & 1),
-            // atom (l >> 1) & 1
-            const int pp = lane >> 2, half = lane & 1, a = (lane >> 1) & 1;
-            const int64_t pg = __shfl_sync(0xffffffffu, ids, (4 * j + pp) & 31);
-            if (lane < 4 * np)
-                bulk_g2s_plain((half ? vs : ks) + a * 8192 + pp * 2048,
-                               p.kv + pg * kPageBytes + half * kHalfPage + a * kAtomBytes, kAtomBytes,
-                               kv_full + 8 * st);
+            {
+                const int st = j % kVS;
+                if (j >= kVS) mbar_wait(v_empty + 8 * st, ((j / kVS) - 1) & 1);
+                const uint32_t vs = v_s + st * kTcKVBytes;
+                if (np < kPB) {
+                    // keys of missing pages are masked; their V rows must be finite
+                    const int per_atom = (kPB - np) * 128;  // 16-byte chunks past page np-1
+                    for (int c = lane; c < 2 * per_atom; c += 32) {
+                        const int aa = c / per_atom, w = c - aa * per_atom;
+                        reinterpret_cast<uint4 *>(smem + (vs - sb) + aa * kAtom + np * 2048)[w] =
+                            make_uint4(0, 0, 0, 0);
+                    }
+                    fence_proxy_async();
+                }
+                if (lane == 0) mbar_expect_tx(v_full + 8 * st, np * kHalfPage);
+                __syncwarp();
+                if (lane < 2 * np)
+                    bulk_g2s_plain(vs + a * kAtom + pp * 2048, src + kHalfPage, kAtomBytes, v_full + 8 * st);
+            }
         }
     } else if (warp == kSoftWarps + 1) {
         // ---------------- MMA issuer ----------------
@@ -225,53 +287,68 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
         // slower than the tensor pipe (tools/ubench/mma_rate.cu, twohalf).
         mbar_wait(q_ready, 0);
         tc_after();
-        auto issue_s = [&](int j) {
-            const int st = j % kTcStages, b = j & 1;
-            mbar_wait(kv_full + 8 * st, (j / kTcStages) & 1);
-            const uint32_t ks = kv_s + 2 * st * kTcKVBytes;
+        // S_h(j) into buffer j % kSBuf of half h
+        auto issue_s_half = [&](int j, int h) {
+            const int b = j % kSBuf;
+            const uint32_t ks = k_s + (j % kKS) * kTcKVBytes;
+            // S_j overwrites the TMEM columns P_{j-kSBuf} occupied: the
+            // tensor pipe runs this warp's MMAs in issue order, so
+            // P.V_{j-kSBuf} (issued earlier) has read them
+            tc_after();
+            const uint32_t qh = q_s + h * kTcQBytes;
+            const uint32_t s_t = tmem + 256 * h + kHeadDim + b * kTcKeys;
+            if (elect_one()) {
 #pragma unroll
-            for (int h = 0; h < NQ; ++h) {
-                // S_j overwrites the TMEM columns P_{j-2} occupied: the
-                // tensor pipe runs this warp's MMAs in issue order, so
-                // P.V_{j-2} (issued earlier) has read them
-                tc_after();
-                const uint32_t qh = q_s + h * kTcQBytes;
-                const uint32_t s_t = tmem + 256 * h + kHeadDim + b * kTcKeys;
-                if (elect_one()) {
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const uint64_t ad = tc_desc(qh + (k >> 2) * (kTcRows * 128) + (k & 3) * 32, 16, 1024);
-                        const uint64_t bd = tc_desc(ks + (k >> 2) * (kTcKeys * 128) + (k & 3) * 32, 16, 1024);
-                        tc_mma_f16(s_t, ad, bd, kIdescS, k > 0);
-                    }
-                    tc_commit_bar(s_full + 8 * (2 * h + b));
+                for (int k = 0; k < 8; ++k) {
+                    const uint64_t ad = tc_desc(qh + (k >> 2) * (kTcRows * 128) + (k & 3) * 32, 16, 1024);
+                    const uint64_t bd = tc_desc(ks + (k >> 2) * kAtom + (k & 3) * 32, 16, 1024);
+                    tc_mma_f16(s_t, ad, bd, kIdescS, k > 0);
                 }
-                __syncwarp();
+                tc_commit_bar(s_full + 8 * (2 * h + b));
+                if (h == NQ - 1) tc_commit_bar(k_empty + 8 * (j % kKS));  // K_j read by S_j
             }
+            __syncwarp();
         };
-        issue_s(0);
-        if (nb > 1) issue_s(1);
+        auto wait_kv = [&](int j) { mbar_wait(k_full + 8 * (j % kKS), (j / kKS) & 1); };
+        for (int j = 0; j < kSBuf && j < nb; ++j) {
+            wait_kv(j);
+#pragma unroll
+            for (int h = 0; h < NQ; ++h) issue_s_half(j, h);
+        }
         for (int j = 0; j < nb; ++j) {
-            const int st = j % kTcStages, b = j & 1;
-            const uint32_t vs = kv_s + (2 * st + 1) * kTcKVBytes;
+            const int st = j % kVS, b = j % kSBuf;
+            const uint32_t vs = v_s + st * kTcKVBytes;
+            const bool more = j + kSBuf < nb;
+            mbar_wait(v_full + 8 * st, (j / kVS) & 1);
 #pragma unroll
             for (int h = 0; h < NQ; ++h) {
-                mbar_wait(p_full + 8 * (2 * h + b), (j >> 1) & 1);
+                mbar_wait(p_full + 8 * (2 * h + b), (j / kSBuf) & 1);
                 tc_after();
                 const uint32_t pt = tmem + 256 * h + kHeadDim + b * kTcKeys;  // P over S_j
                 if (elect_one()) {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const uint64_t bd = tc_desc(vs + k * 2048, kTcKeys * 128, 1024);
+                    for (int k = 0; k < kTcKeys / 16; ++k) {
+                        const uint64_t bd = tc_desc(vs + k * 2048, kAtom, 1024);
                         tc_mma_f16_ta(tmem + 256 * h, pt + k * 8, bd, kIdescPV, (j > 0 || k > 0) ? 1u : 0u);
                     }
                     tc_commit_bar(o_done + 8 * (2 * h + b));
                 }
                 __syncwarp();
+                if (kSBuf == 1 && more) {
+                    // one S buffer per half: S_h(j+1) right behind P.V_h(j),
+                    // so half h's softmax restarts while the other half's
+                    // MMAs run
+                    if (h == 0) wait_kv(j + 1);
+                    issue_s_half(j + 1, h);
+                }
             }
-            if (elect_one()) tc_commit_bar(kv_empty + 8 * st);
+            if (elect_one()) tc_commit_bar(v_empty + 8 * st);  // V_j read by P.V_j
             __syncwarp();
-            if (j + 2 < nb) issue_s(j + 2);
+            if (kSBuf == 2 && more) {
+                wait_kv(j + 2);
+#pragma unroll
+                for (int h = 0; h < NQ; ++h) issue_s_half(j + 2, h);
+            }
         }
     } else {
         // ---------------- softmax / correction / epilogue (row = thread) ----------------
@@ -319,35 +396,37 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
         const uint32_t o_t = tmem + 256 * h + lane_base, s_t = o_t + kHeadDim;
         float m_used = -INFINITY, l = 0.f;
         for (int j = 0; j < nb; ++j) {
-            const int b = j & 1, hb = 2 * h + b;
-            mbar_wait(s_full + 8 * hb, (j >> 1) & 1);
+            const int b = j % kSBuf, hb = 2 * h + b;
+            mbar_wait(s_full + 8 * hb, (j / kSBuf) & 1);
             tc_after();
-            uint32_t sr[2][32];
-            tc_ld32(s_t + b * kTcKeys, sr[0]);
-            tc_ld32(s_t + b * kTcKeys + 32, sr[1]);
+            constexpr int kC = kTcKeys / 32;  // 32-column groups of S
+            uint32_t sr[kC][32];
+#pragma unroll
+            for (int hh = 0; hh < kC; ++hh) tc_ld32(s_t + b * kTcKeys + 32 * hh, sr[hh]);
             tc_wait_ld();
-            const int kb0 = (pg0 + 4 * j) * kPageTokens;
+            const int kb0 = (pg0 + kPB * j) * kPageTokens;
             // raw scores: the scale is folded into the exponent's FFMA; the
             // mask only runs on blocks crossing a row's diagonal or the range
             // end (warp-uniform test on the half's smallest row position)
             if (kb0 + kTcKeys - 1 > pos_min || kb0 + kTcKeys > kv_lim) {
 #pragma unroll
-                for (int hh = 0; hh < 2; ++hh)
+                for (int hh = 0; hh < kC; ++hh)
 #pragma unroll
                     for (int c = 0; c < 32; ++c) {
                         const int key = kb0 + hh * 32 + c;
                         if (key > pos || key >= kv_lim) sr[hh][c] = __float_as_uint(-INFINITY);
                     }
             }
-            float mxs[8];
+            float mxs[4];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) mxs[i] = -INFINITY;
+            for (int i = 0; i < 4; ++i) mxs[i] = -INFINITY;
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh)
+            for (int hh = 0; hh < kC; ++hh)
 #pragma unroll
-                for (int c = 0; c < 32; ++c) mxs[c & 7] = fmaxf(mxs[c & 7], __uint_as_float(sr[hh][c]));
-            const float mx = fmaxf(fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3])),
-                                   fmaxf(fmaxf(mxs[4], mxs[5]), fmaxf(mxs[6], mxs[7]))) * scale;
+                for (int c = 0; c < 32; c += 2)
+                    mxs[(c >> 1) & 3] = fmax3(mxs[(c >> 1) & 3], __uint_as_float(sr[hh][c]),
+                                              __uint_as_float(sr[hh][c + 1]));
+            const float mx = fmax3(fmaxf(mxs[0], mxs[1]), mxs[2], mxs[3]) * scale;
             float alpha = 1.f;
             const bool grow = mx > m_used + kTcRescale;
             if (grow) {
@@ -355,9 +434,37 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
                 m_used = mx;
                 l *= alpha;
             }
+            const float mu = m_used == -INFINITY ? 0.f : m_used;
+            uint64_t ls2[2] = {f2(0.f, 0.f), f2(0.f, 0.f)};
+            const uint64_t scale2 = f2(scale, scale), nmu2 = f2(-mu, -mu);
+            // P_j (f16, 2 keys per 32-bit column) over the S_j columns in
+            // TMEM: the A operand of P.V_j; one 32-column S group -> 16
+            // packed P columns at a time, so each group's registers die as
+            // soon as it is stored
+#pragma unroll
+            for (int hh = 0; hh < kC; ++hh) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    float x0, x1;
+                    f2_split(ffma2(f2(__uint_as_float(sr[hh][2 * c]), __uint_as_float(sr[hh][2 * c + 1])),
+                                   scale2, nmu2), x0, x1);
+                    const float e0 = fast_exp2(x0), e1 = fast_exp2(x1);
+                    const uint64_t e2 = f2(e0, e1);
+                    ls2[c & 1] = fadd2(ls2[c & 1], e2);
+                    pk[c] = pack_f16(e0, e1);
+                }
+                tc_st16(s_t + b * kTcKeys + 16 * hh, pk);
+            }
+            tc_wait_st();
+            float ls[4];
+            f2_split(ls2[0], ls[0], ls[1]);
+            f2_split(ls2[1], ls[2], ls[3]);
             if (j > 0 && __any_sync(0xffffffffu, grow)) {
                 // rescale this warp's O rows once P_{j-1} . V_{j-1} landed
-                mbar_wait(o_done + 8 * (2 * h + ((j - 1) & 1)), ((j - 1) >> 1) & 1);
+                // (after P_j is stored: S_j's registers are dead by now;
+                // P.V_j waits for p_full below)
+                mbar_wait(o_done + 8 * (2 * h + ((j - 1) % kSBuf)), ((j - 1) / kSBuf) & 1);
                 tc_after();
 #pragma unroll
                 for (int cc = 0; cc < 4; ++cc) {
@@ -370,20 +477,6 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
                 }
                 tc_wait_st();
             }
-            const float mu = m_used == -INFINITY ? 0.f : m_used;
-            float ls[4] = {0.f, 0.f, 0.f, 0.f};
-            // P_j (f16, 2 keys per 32-bit column) over the S_j columns in
-            // TMEM: the A operand of P.V_j
-            uint32_t pk[32];
-#pragma unroll
-            for (int c = 0; c < 32; ++c) {
-                const float e0 = fast_exp2(fmaf(__uint_as_float(sr[c >> 4][(2 * c) & 31]), scale, -mu));
-                const float e1 = fast_exp2(fmaf(__uint_as_float(sr[c >> 4][(2 * c + 1) & 31]), scale, -mu));
-                ls[c & 3] += e0 + e1;
-                pk[c] = pack_f16(e0, e1);
-            }
-            tc_st32(s_t + b * kTcKeys, pk);
-            tc_wait_st();
             l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
             tc_before();
             __syncwarp();
@@ -391,7 +484,7 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
         }
         // ---- epilogue: O / l (or the split partial) ----
         grid_launch_dependents();  // the combine launch (PDL) may be scheduled now
-        mbar_wait(o_done + 8 * (2 * h + ((nb - 1) & 1)), ((nb - 1) >> 1) & 1);
+        mbar_wait(o_done + 8 * (2 * h + ((nb - 1) % kSBuf)), ((nb - 1) / kSBuf) & 1);
         tc_after();
         const float inv = l > 0.f ? 1.f / l : 0.f;
         const int slot = p.tile_slot[t];

@@ -22,8 +22,9 @@ from . import _native as N
 from .core import ValidationError
 
 # kernel variants: 0 = tcgen05 (TMEM accumulators, two 128-row halves per
-# tile), 1 = mma.sync (64-row tiles), 2 = tcgen05 with one 128-row half
-VARIANT_ROWS = {0: 256, 1: 64, 2: 128}
+# tile, 64-key blocks), 1 = mma.sync (64-row tiles), 2 = tcgen05 with one
+# 128-row half, 3 = tcgen05, two halves, 128-key blocks
+VARIANT_ROWS = {0: 256, 1: 64, 2: 128, 3: 256}
 DEFAULT_VARIANT = 0
 
 

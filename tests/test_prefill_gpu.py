@@ -87,7 +87,7 @@ def _run_case(qpk, starts, lens, seed, target_units=None, q_pad=3, out_dtype=tor
 
 
 # 0: tcgen05 / TMEM, 2 x 128-row halves; 1: mma.sync, 64-row tiles; 2: tcgen05, 128 rows
-VARIANTS = [0, 1, 2]
+VARIANTS = [0, 1, 2, 3]
 
 
 @pytest.mark.parametrize("variant", VARIANTS)

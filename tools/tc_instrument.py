@@ -7,18 +7,20 @@ p = "paper_2511_14116_b200/csrc/prefill_tc.cuh"
 s = open(p).read()
 mode = sys.argv[1]
 if "timeline" in mode:
-    s = s.replace('''    const int nb = (npg + 3) >> 2;  // 64-key blocks
-''', '''    const int nb = (npg + 3) >> 2;  // 64-key blocks
+    s = s.replace('''    const int nb = (npg + kPB - 1) / kPB;  // key blocks
+''', '''    const int nb = (npg + kPB - 1) / kPB;  // key blocks
     long long *dbgp = reinterpret_cast<long long *>(p.part_lse) + 1000000 + blockIdx.x * 8;
     auto gtm = []() { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return (long long)t; };
     if (threadIdx.x == 0) { unsigned sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm)); dbgp[0] = gtm(); dbgp[4] = sm; dbgp[5] = nb; }
 ''', 1)
-    s = s.replace('''        issue_s(0);
-        if (nb > 1) issue_s(1);''', '''        if (lane == 0) dbgp[1] = gtm();
-        issue_s(0);
-        if (nb > 1) issue_s(1);''', 1)
-    s = s.replace('''            if (j + 2 < nb) issue_s(j + 2);
-        }''', '''            if (j + 2 < nb) issue_s(j + 2);
+    s = s.replace('''        for (int j = 0; j < kSBuf && j < nb; ++j) {
+            wait_kv(j);''', '''        if (lane == 0) dbgp[1] = gtm();
+        for (int j = 0; j < kSBuf && j < nb; ++j) {
+            wait_kv(j);''', 1)
+    s = s.replace('''                for (int h = 0; h < NQ; ++h) issue_s_half(j + 2, h);
+            }
+        }''', '''                for (int h = 0; h < NQ; ++h) issue_s_half(j + 2, h);
+            }
         }
         if (lane == 0) dbgp[2] = gtm();''', 1)
     s = s.replace('''    tc_before();
@@ -34,19 +36,18 @@ if "timeline" in mode:
     assert s.count("dbgp") >= 6, "timeline patch failed"
 if "waits" in mode:
     # cycles the MMA warp spends waiting for K/V (kv_full) and for P (p_full)
-    s = s.replace("""        auto issue_s = [&](int j) {
-            const int st = j % kTcStages, b = j & 1;
-            mbar_wait(kv_full + 8 * st, (j / kTcStages) & 1);""", """        long long w_kv = 0, w_p = 0, c_loop0 = clock64();
-        auto issue_s = [&](int j) {
-            const int st = j % kTcStages, b = j & 1;
-            { long long c0 = clock64(); mbar_wait(kv_full + 8 * st, (j / kTcStages) & 1); w_kv += clock64() - c0; }""", 1)
-    s = s.replace("""                mbar_wait(p_full + 8 * (2 * h + b), (j >> 1) & 1);
+    s = s.replace("""        auto wait_kv = [&](int j) { mbar_wait(k_full + 8 * (j % kKS), (j / kKS) & 1); };""", """        long long w_kv = 0, w_p = 0, c_loop0 = clock64();
+        auto wait_kv = [&](int j) { long long c0 = clock64(); mbar_wait(k_full + 8 * (j % kKS), (j / kKS) & 1); w_kv += clock64() - c0; };""", 1)
+    s = s.replace("""                mbar_wait(p_full + 8 * (2 * h + b), (j / kSBuf) & 1);
                 tc_after();
-                const uint32_t pt""", """                { long long c0 = clock64(); mbar_wait(p_full + 8 * (2 * h + b), (j >> 1) & 1); w_p += clock64() - c0; }
+                const uint32_t pt""", """                { long long c0 = clock64(); mbar_wait(p_full + 8 * (2 * h + b), (j / kSBuf) & 1); w_p += clock64() - c0; }
                 tc_after();
                 const uint32_t pt""", 1)
     s = s.replace("""        if (lane == 0) dbgp[2] = gtm();""", """        if (lane == 0) { dbgp[2] = gtm(); dbgp[6] = w_kv; dbgp[7] = w_p; dbgp[5] |= (clock64() - c_loop0) << 16; }""", 1)
-    assert s.count("w_kv") == 3, s.count("w_kv")
+    s = s.replace("""            mbar_wait(v_full + 8 * st, (j / kVS) & 1);""", """            { long long c0 = clock64(); mbar_wait(v_full + 8 * st, (j / kVS) & 1); w_v += clock64() - c0; }""", 1)
+    s = s.replace("long long w_kv = 0, w_p = 0,", "long long w_kv = 0, w_v = 0, w_p = 0,", 1)
+    s = s.replace("dbgp[6] = w_kv;", "dbgp[6] = w_kv | (w_v << 32);", 1)
+    assert s.count("w_kv") == 3 and s.count("w_v +=") == 1, s.count("w_kv")
 if "prologue" in mode:
     # dbg[6] = after setup barrier (thread 0), dbg[7] = softmax warp 0 Q rows stored
     s = s.replace("""    const uint32_t tmem = *tmem_slot;
@@ -71,6 +72,12 @@ if "qload" in mode:
 """, """    const uint32_t tmem = *tmem_slot;
     if (threadIdx.x == 0) dbgp[6] = gtm();
 """, 1)
+if "noexp" in mode:
+    # ablation: the exponentials replaced by an FFMA (wrong P, same data flow)
+    old = "fast_exp2("
+    n = s.count(old)
+    i = s.index("uint32_t pk[32];")
+    s = s[:i] + s[i:].replace("fast_exp2(", "(1.0f + 0.5f * ", 2)
 if "nosoftmax" in mode:
     old = '''            uint32_t sr[2][32];
             tc_ld32(s_t + b * kTcKeys, sr[0]);'''

@@ -4,6 +4,7 @@ import numpy as np, torch
 from paper_2511_14116_b200.kvcache import PagedKVCache, RankWork
 from paper_2511_14116_b200.prefill import PrefillLaunch
 cnt, ln, st = [int(x) for x in sys.argv[1:4]] if len(sys.argv) > 3 else (1, 2048, 8192)
+variant = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 work = RankWork.build(np.zeros((1, 1), np.int32), 0, {r: 0 for r in range(cnt)}, cnt)
 cache = PagedKVCache(work, st + ln, 8)
 cache.pool.view(torch.bfloat16).normal_()
@@ -11,7 +12,7 @@ stride = 10 * 128
 q = torch.randn((cnt * ln, stride), device="cuda").to(torch.bfloat16)
 out = torch.empty_like(q)
 row0 = np.arange(cnt) * ln * stride
-L = PrefillLaunch(cache, np.arange(cnt), [st] * cnt, [ln] * cnt, row0, row0, variant=0)
+L = PrefillLaunch(cache, np.arange(cnt), [st] * cnt, [ln] * cnt, row0, row0, variant=variant)
 L.part_lse = torch.zeros(max(4_000_000, L.part_lse.numel() if L.part_lse is not None else 0), device="cuda")
 for _ in range(3): L(q, stride, out, stride)
 torch.cuda.synchronize()
@@ -25,8 +26,9 @@ t0 = d[:, 0].min()
 st_, mma0, mma1, end, sm, nb = [d[:, i] for i in range(6)]
 cyc = nb >> 16; nb = nb & 0xffff
 if cyc.any():
-    print("MMA warp per block: loop cycles %.0f, kv_full wait %.0f, p_full wait %.0f" % (
-        np.median(cyc / nb), np.median(d[:, 6] / nb), np.median(d[:, 7] / nb)))
+    print("MMA warp per block: loop cycles %.0f, k_full wait %.0f, v_full wait %.0f, p_full wait %.0f" % (
+        np.median(cyc / nb), np.median((d[:, 6] & 0xffffffff) / nb), np.median((d[:, 6] >> 32) / nb),
+        np.median(d[:, 7] / nb)))
 if not cyc.any() and d[:, 6].any():
     print("setup us %.2f, Q stored us %.2f (from CTA start)" % (np.median(d[:, 6] - st_) / 1e3, np.median(d[:, 7] - st_) / 1e3))
 print("tiles", n, "kernel span us", (end.max() - t0) / 1e3)
