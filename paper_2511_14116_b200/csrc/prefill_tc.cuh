@@ -123,6 +123,26 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
     return d;
 }
 
+// 2^x on the FMA pipe for a pair (FA4's MUFU offload): x = n + f with n =
+// round(x), f in [-0.5, 0.5]; near-minimax cubic for 2^f (max rel err
+// 7.5e-5, below f16's half ulp); n added to the exponent field.  x >= -125
+// keeps that field positive (such P underflow to 0 in f16 anyway).
+__device__ __forceinline__ void exp2_fma2(float x0, float x1, float &e0, float &e1) {
+    const uint64_t x = f2(fmaxf(x0, -125.f), fmaxf(x1, -125.f));
+    const uint64_t magic = f2(12582912.f, 12582912.f);  // 1.5 * 2^23
+    const uint64_t t = fadd2(x, magic);
+    const uint64_t r = fadd2(t, f2(-12582912.f, -12582912.f));  // round(x)
+    const uint64_t f = fadd2(x, r ^ 0x8000000080000000ull);        // x - round(x)
+    uint64_t p = ffma2(f2(0.05517166f, 0.05517166f), f, f2(0.24261114f, 0.24261114f));
+    p = ffma2(p, f, f2(0.69326097f, 0.69326097f));
+    p = ffma2(p, f, f2(0.99992806f, 0.99992806f));
+    float t0, t1, p0, p1;
+    f2_split(t, t0, t1);
+    f2_split(p, p0, p1);
+    e0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+    e1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+}
+
 __device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -449,7 +469,13 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
                     float x0, x1;
                     f2_split(ffma2(f2(__uint_as_float(sr[hh][2 * c]), __uint_as_float(sr[hh][2 * c + 1])),
                                    scale2, nmu2), x0, x1);
-                    const float e0 = fast_exp2(x0), e1 = fast_exp2(x1);
+                    float e0, e1;
+                    if (BK == 128 && (c & 3) == 3) {
+                        exp2_fma2(x0, x1, e0, e1);  // a quarter of the pairs off the MUFU
+                    } else {
+                        e0 = fast_exp2(x0);
+                        e1 = fast_exp2(x1);
+                    }
                     const uint64_t e2 = f2(e0, e1);
                     ls2[c & 1] = fadd2(ls2[c & 1], e2);
                     pk[c] = pack_f16(e0, e1);
