@@ -25,7 +25,7 @@ from .core import ValidationError
 # tile, 64-key blocks), 1 = mma.sync (64-row tiles), 2 = tcgen05 with one
 # 128-row half, 3 = tcgen05, two halves, 128-key blocks
 VARIANT_ROWS = {0: 256, 1: 64, 2: 128, 3: 256}
-DEFAULT_VARIANT = 0
+DEFAULT_VARIANT = 3
 
 
 def default_target_units(device_index: int, variant: int = DEFAULT_VARIANT) -> int:

@@ -78,6 +78,13 @@ if "noexp" in mode:
     n = s.count(old)
     i = s.index("uint32_t pk[32];")
     s = s[:i] + s[i:].replace("fast_exp2(", "(1.0f + 0.5f * ", 2)
+if "epi" in mode:
+    # dbg[6] = last P.V landed (softmax thread 0), dbg[7] = partial stores issued
+    s = s.replace("""        mbar_wait(o_done + 8 * (2 * h + ((nb - 1) % kSBuf)), ((nb - 1) / kSBuf) & 1);""", """        mbar_wait(o_done + 8 * (2 * h + ((nb - 1) % kSBuf)), ((nb - 1) / kSBuf) & 1);
+        if (threadIdx.x == 0) dbgp[6] = gtm();""", 1)
+    s = s.replace("""        if (slot >= 0) p.part_lse[(int64_t)slot * rows + R] = l > 0.f ? m_used + __log2f(l) : -INFINITY;""", """        if (slot >= 0) p.part_lse[(int64_t)slot * rows + R] = l > 0.f ? m_used + __log2f(l) : -INFINITY;
+        if (threadIdx.x == 0) dbgp[7] = gtm();""", 1)
+    assert s.count("dbgp[6]") == 1 and s.count("dbgp[7]") == 1
 if "nosoftmax" in mode:
     old = '''            uint32_t sr[2][32];
             tc_ld32(s_t + b * kTcKeys, sr[0]);'''
