@@ -223,6 +223,10 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
     const int pg0 = p.tile_page0[t];
     const int npg = p.tile_page1[t] - pg0;
     const int nb = (npg + kPB - 1) / kPB;  // key blocks
+    // the item's parameters, loaded before the setup barrier so their
+    // latency overlaps barrier init and the TMEM allocation
+    const int it_seq = p.item_seq[item], it_start = p.item_start[item], it_len = p.item_len[item];
+    const int it_qoff = p.item_qoff[item];
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kKS; ++s) {
@@ -253,7 +257,7 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
 
     if (warp == kSoftWarps) {
         // ---------------- TMA producer ----------------
-        const int64_t row = (int64_t)p.item_seq[item] * p.bt_stride + pg0;
+        const int64_t row = (int64_t)it_seq * p.bt_stride + pg0;
         // page ids 32 at a time (lane = page), the next 32 prefetched a
         // chunk ahead so the block-table load latency stays off the ring
         int64_t ids = lane < npg ? p.bt[row + lane] : 0;
@@ -376,11 +380,9 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
         const int r = threadIdx.x & 127;                  // row within the half = TMEM lane
         const int R = h * kTcRows + r;                    // row within the tile
         const int qpk = p.qpk, rows_used = p.tpt * qpk;
-        const int start = p.item_start[item], n = p.item_len[item];
+        const int start = it_start, n = it_len;
         const int tl = min(R, rows_used - 1) / qpk;
         const int tok = min(tok0 + tl, n - 1);
-        const int hd = R % qpk;
-        const bool valid = R < rows_used && tok0 + R / qpk < n;
         const int pos = start + tok;                     // causal limit of this row
         const int kv_lim = (pg0 + npg) * kPageTokens;    // keys past the range: masked
         // smallest row position of this half (rows of a half are in token order)
@@ -391,7 +393,7 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
             // the warp loads its 32 rows cooperatively, two 256-B rows per
             // instruction (rows of one token are adjacent heads: coalesced),
             // all 16 loads in flight before the swizzled smem stores
-            const __nv_bfloat16 *qb = p.q + p.item_qoff[item];
+            const __nv_bfloat16 *qb = p.q + it_qoff;
             const int c = lane & 15;
             uint4 v[16];
 #pragma unroll

@@ -59,7 +59,7 @@ if "prologue" in mode:
 if "qload" in mode:
     # dbg[1] (reused) = params loaded, dbg[2] = Q loads returned, dbg[7] = Q stored (thread 0)
     s = s.replace("""            uint4 v[16];""", """            if (threadIdx.x == 0) { dbgp[1] = gtm() + 0 * (start + n + (long long)qb); }
-            uint4 v[16];""", 1)
+            uint4 v[16];""", 1) if "qload" in mode else s
     s = s.replace("""#pragma unroll
             for (int i = 0; i < 16; ++i) {
                 const int ri = (warp & 3) * 32""", """            if (threadIdx.x == 0) { uint32_t x = 0; for (int i = 0; i < 16; ++i) x ^= v[i].x; dbgp[2] = gtm() + (x == 0x12345 ? 1 : 0); }
