@@ -10,5 +10,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:decode \
     -s 40 -c 1 -o $OUT/decode_full $BENCH > $OUT/full_bench.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:prefill_tc \
-    -s 3 -c 1 -o $OUT/prefill_full python tools/prefill_bench.py --cases 1x2048@8192 --iters 2 > $OUT/full_prefill.log 2>&1
+    -s 3 -c 1 -o $OUT/prefill_full python tools/prefill_bench.py --variant 3 --cases 1x2048@8192 --iters 2 > $OUT/full_prefill.log 2>&1
 ls -la $OUT
