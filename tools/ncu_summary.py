@@ -141,7 +141,7 @@ def main():
         flops = 4 * 128 * 8 * vis
         summ = {
             "source": f"profiles/{tag}_prefill_full.ncu-rep (ncu --set full --clock-control none "
-                      "-k regex:prefill_tc -s 3 -c 1, tools/prefill_bench.py --cases "
+                      "-k regex:prefill_tc -s 3 -c 1, tools/prefill_bench.py --variant 3 --cases "
                       "1x2048@8192)",
             "kernel": m.get("Kernel Name", ("prefill_kernel", ""))[0],
             "duration_us": dur * 1e6,
