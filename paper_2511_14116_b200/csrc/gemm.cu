@@ -206,7 +206,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint32_t bar_empty = bar_full + 8 * kGemmStages;
     const uint32_t bar_acc_full = bar_empty + 8 * kGemmStages;   // [2]
     const uint32_t bar_acc_empty = bar_acc_full + 16;            // [2]
-    const uint32_t bar_red = bar_acc_empty + 16;                 // split-tile gather
     __shared__ uint32_t s_tmem;
 
 
@@ -226,7 +225,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             mbar_init(bar_acc_full + 8 * b, 1);
             mbar_init(bar_acc_empty + 8 * b, 128);
         }
-        mbar_init(bar_red, 1);
         fence_barrier_init();
         fence_proxy_async();
     }
@@ -332,12 +330,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
         } else {
             // ---------------- epilogue (warps 0-3) ----------------
-            const int tid = threadIdx.x;  // 0..127
             const int m = warp * 32 + lane;
             int seg = 0;
             int64_t u = u0;
-            int pend[2], n_pend = 0;  // split tiles (only the range's first / last)
-            int n_red = 0;            // uses of bar_red (phase parity)
             while (u < u1) {
                 const int t = (int)(u / nk);
                 const int64_t tb = (int64_t)t * nk, te = tb + nk;
@@ -363,87 +358,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     gemm_epilogue(p, acc, t, m, up);
                     named_bar_sync(2, 128);  // 'up' staging reused by the next segment
                 } else {
-                    // split tile: publish this CTA's fp32 partial now (never
-                    // blocks); the reduction runs after every segment of this
-                    // CTA has been published, so no CTA waits on a chain
+                    // split tile: this CTA's fp32 partial goes to slot
+                    // tile + cta; gemm_reduce_kernel (the next launch, PDL)
+                    // sums a tile's partials in CTA order -- no CTA of this
+                    // grid ever waits for another
                     const int64_t slot = (int64_t)t + c;
                     float *wsl = p.ws + slot * (kRowsN * kTileM);
 #pragma unroll
                     for (int n = 0; n < kRowsN; ++n) __stcg(wsl + n * kTileM + m, acc[n]);
-                    __threadfence();
-                    named_bar_sync(2, 128);
-                    if (tid == 0) atomicAdd(p.sems + t, 1);
-                    if (n_pend < 2) pend[n_pend++] = t;
                 }
                 if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 8 + 3] = gtimer();
                 u = seg_end;
                 ++seg;
-            }
-            // Split tiles: once every contributor published, contributor i
-            // reduces rows [64i/nseg, 64(i+1)/nseg) over all partials in CTA
-            // order (deterministic) and applies the epilogue; the last
-            // finisher resets the two per-tile counters.  Waits only target
-            // publications, which never block, so the grid cannot deadlock.
-            for (int k = 0; k < n_pend; ++k) {
-                const int t = pend[k];
-                const int64_t tb = (int64_t)t * nk, te = tb + nk;
-                int32_t *pub = p.sems + t, *fin = p.sems + p.tiles + t;
-                const int64_t clo = gemm_owner(tb, C, U), chi = gemm_owner(te - 1, C, U);
-                int nseg = 0, rank = 0;
-                for (int64_t s = clo; s <= chi; ++s) {
-                    const bool live = U >= C || gemm_live(s, C, U);
-                    nseg += live;
-                    rank += live && s < c;
-                }
-                const int r_lo = rank * kRowsN / nseg, r_hi = (rank + 1) * kRowsN / nseg;
-                const int R = min(r_hi, p.rows) - r_lo;
-                // the stage ring is idle now (every MMA of this CTA is done):
-                // one bulk copy per contributor pulls rows [r_lo, r_hi) of its
-                // partial, all in flight together -> one L2 round trip
-                float *red = reinterpret_cast<float *>(smem);
-                if (tid == 0) {
-                    while (ld_acquire(pub) < nseg) __nanosleep(32);
-                    asm volatile("fence.proxy.async.global;" ::: "memory");
-                    if (R > 0) {
-                        mbar_expect_tx(bar_red, (uint32_t)(nseg * R * kTileM * 4));
-                        int idx = 0;
-                        for (int64_t s = clo; s <= chi; ++s) {
-                            if (U < C && !gemm_live(s, C, U)) continue;
-                            bulk_g2s(sbase + idx * R * kTileM * 4,
-                                     p.ws + (t + s) * (kRowsN * kTileM) + r_lo * kTileM,
-                                     R * kTileM * 4, bar_red, policy_evict_first());
-                            ++idx;
-                        }
-                    }
-                }
-                if (R > 0) {
-                    mbar_wait(bar_red, (uint32_t)(n_red & 1));
-                    ++n_red;
-                    const bool swiglu = p.epilogue == EPI_SWIGLU;
-                    for (int r = 0; r < R; ++r) {
-                        const int n = r_lo + r;
-                        float g = 0.f, uu = 0.f;
-                        for (int idx = 0; idx < nseg; ++idx) {  // CTA order
-                            const float *row = red + (idx * R + r) * kTileM;
-                            g += row[m];
-                            if (swiglu && m < 64) uu += row[64 + m];
-                        }
-                        if (swiglu) {
-                            if (m < 64)
-                                p.out[n * p.ld_out + t * 64 + m] = __float2bfloat16_rn(silu(g) * uu);
-                        } else {
-                            const int64_t col = (int64_t)t * kTileM + m;
-                            if (p.epilogue == EPI_RESIDUAL)
-                                g += __bfloat162float(p.res[n * p.ld_res + col]);
-                            p.out[n * p.ld_out + col] = __float2bfloat16_rn(g);
-                        }
-                    }
-                }
-                named_bar_sync(2, 128);
-                if (tid == 0 && atomicAdd(fin, 1) == nseg - 1) {
-                    *pub = 0;
-                    *fin = 0;
-                }
             }
             if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 8 + 3] = gtimer();
         }
@@ -454,6 +380,57 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (warp == 0) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
+    }
+}
+
+// Split tiles of a stream-K launch: block (tile, 8-row group); thread m sums
+// column m of the tile over the contributors' partials in CTA order
+// (deterministic) and applies the epilogue.  Blocks of whole tiles exit.
+// Launched with PDL right behind gemm_skinny_kernel: scheduled during its
+// tail, waits in griddepcontrol.wait for its partials.
+constexpr int kRedRows = 8;
+
+__global__ void __launch_bounds__(kTileM) gemm_reduce_kernel(const GemmParams p, int32_t grid) {
+    const int t = blockIdx.x, r0 = blockIdx.y * kRedRows, m = threadIdx.x;
+    const int nk = p.K / kStepK;
+    const int64_t C = grid, U = p.n_units;
+    const int64_t tb = (int64_t)t * nk, te = tb + nk;
+    const int64_t clo = gemm_owner(tb, C, U), chi = gemm_owner(te - 1, C, U);
+    grid_launch_dependents();
+    if (clo == chi || r0 >= p.rows) return;  // whole tile: the GEMM stored it
+    const bool swiglu = p.epilogue == EPI_SWIGLU;
+    if (swiglu && m >= 64) return;
+    grid_dependency_wait();
+    float g[kRedRows], uu[kRedRows];
+#pragma unroll
+    for (int r = 0; r < kRedRows; ++r) g[r] = uu[r] = 0.f;
+    for (int64_t s = clo; s <= chi; ++s) {  // CTA order
+        if (U < C && !gemm_live(s, C, U)) continue;
+        const float *src = p.ws + (t + s) * (kRowsN * kTileM) + r0 * kTileM + m;
+        float vg[kRedRows], vu[kRedRows];
+#pragma unroll
+        for (int r = 0; r < kRedRows; ++r) {
+            vg[r] = __ldcg(src + r * kTileM);
+            vu[r] = swiglu ? __ldcg(src + r * kTileM + 64) : 0.f;
+        }
+#pragma unroll
+        for (int r = 0; r < kRedRows; ++r) {
+            g[r] += vg[r];
+            uu[r] += vu[r];
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < kRedRows; ++r) {
+        const int n = r0 + r;
+        if (n >= p.rows) break;
+        if (swiglu) {
+            p.out[n * p.ld_out + t * 64 + m] = __float2bfloat16_rn(silu(g[r]) * uu[r]);
+        } else {
+            const int64_t col = (int64_t)t * kTileM + m;
+            float v = g[r];
+            if (p.epilogue == EPI_RESIDUAL) v += __bfloat162float(p.res[n * p.ld_res + col]);
+            p.out[n * p.ld_out + col] = __float2bfloat16_rn(v);
+        }
     }
 }
 
@@ -571,5 +548,13 @@ extern "C" int fs_gemm_skinny(const void *x, int64_t ld_x, int32_t rows, int32_t
     lc.attrs = attr;
     lc.numAttrs = 1;
     FS_CUDA(cudaLaunchKernelEx(&lc, gemm_skinny_kernel, mw, mx, prm));
+    // the split-tile reduction (blocks of whole tiles exit at once)
+    {
+        cudaLaunchConfig_t lr = lc;
+        lr.gridDim = dim3(prm.tiles, (rows + kRedRows - 1) / kRedRows);
+        lr.blockDim = dim3(kTileM);
+        lr.dynamicSmemBytes = 0;
+        FS_CUDA(cudaLaunchKernelEx(&lr, gemm_reduce_kernel, prm, (int32_t)sms));
+    }
     return FS_OK;
 }
