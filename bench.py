@@ -686,6 +686,10 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        if not shared and local_rank >= torch.cuda.device_count():
+            raise SystemExit(f"bench.py: rank {rank} needs GPU {local_rank} but only "
+                             f"{torch.cuda.device_count()} visible (one process per GPU; "
+                             f"FS_BENCH_SHARED_GPU=1 runs every rank on cuda:0 for testing)")
         torch.cuda.set_device(local_rank)
         if shared:
             dist.init_process_group("gloo")
