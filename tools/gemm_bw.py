@@ -20,8 +20,11 @@ for name, (K, N) in shapes.items():
     x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     res = {}
-    for impl in ("cublas", "tcgen05"):
-        if impl == "tcgen05":
+    for impl in ("cublas", "cublas_nt", "tcgen05"):
+        if impl == "cublas_nt":
+            wts = [w.t().contiguous() for w in ws]  # [N, K]: x @ W^T (the TN layout)
+            f = lambda i: torch.nn.functional.linear(x, wts[i], out=out) if False else torch.matmul(x, wts[i].t(), out=out)
+        elif impl == "tcgen05":
             if N % 128 or K % 64:
                 continue
             pw = [PackedWeight(w) for w in ws]
@@ -46,6 +49,8 @@ for name, (K, N) in shapes.items():
         del g
         if impl == "tcgen05":
             del pw
+        if impl == "cublas_nt":
+            del wts
     print(f"{name:14s} K {K:5d} N {N:5d}: " + "  ".join(
         f"{k} {v[0]:6.1f} us {v[1]:6.0f} GB/s" for k, v in res.items()), flush=True)
     del ws
