@@ -133,3 +133,21 @@ def test_prefill_tile_planner():
                                          qpk, variant, 1, 1, one, one, one, one, one, C.byref(nt), 1,
                                          one, one, one, one, C.byref(nc), C.byref(ns))
         assert rc == N.FS_EVALIDATION
+
+
+def test_prefill_tile_planner_makespan():
+    """The split size minimises the list-scheduling makespan on target_units
+    slots: one slot -> no split at all (every token tile whole); many slots
+    -> the minimum 32-page splits; 148 slots on one long chunk -> more tiles
+    than slots would idle fewer SMs than one wave of 64 unsplit tiles."""
+    from paper_2511_14116_b200.prefill import PrefillTilePlan
+    one = PrefillTilePlan([8192], [2048], 8, 1, 3)
+    assert one.n_comb == 0 and one.n_tiles == 2048 // 32
+    many = PrefillTilePlan([8192], [2048], 8, 100000, 3)
+    widths = many.tiles[3] - many.tiles[2]
+    assert widths.max() <= 2 * 32 and many.n_comb == 2048 // 32
+    sm = PrefillTilePlan([8192], [2048], 8, 148, 3)
+    assert sm.n_tiles > 148 and sm.n_comb == 64
+    # every variant of the same rows plans the same tiles
+    v0 = PrefillTilePlan([8192], [2048], 8, 148, 0)
+    assert (v0.tiles == sm.tiles).all()
