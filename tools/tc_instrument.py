@@ -85,6 +85,34 @@ if "epi" in mode:
     s = s.replace("""        if (slot >= 0) p.part_lse[(int64_t)slot * rows + R] = l > 0.f ? m_used + __log2f(l) : -INFINITY;""", """        if (slot >= 0) p.part_lse[(int64_t)slot * rows + R] = l > 0.f ? m_used + __log2f(l) : -INFINITY;
         if (threadIdx.x == 0) dbgp[7] = gtm();""", 1)
     assert s.count("dbgp[6]") == 1 and s.count("dbgp[7]") == 1
+if "smphase" in mode:
+    # softmax thread 0 of each half: accumulated cycles per phase (wait for S,
+    # TMEM load, max, exp + P store, rest) -> dbg slots 8.. of a second area
+    s = s.replace("""        float m_used = -INFINITY, l = 0.f;
+        for (int j = 0; j < nb; ++j) {""", """        float m_used = -INFINITY, l = 0.f;
+        long long ph_w = 0, ph_ld = 0, ph_mx = 0, ph_ex = 0, ph_rest = 0, c_prev = clock64();
+        for (int j = 0; j < nb; ++j) {""", 1)
+    s = s.replace("""            mbar_wait(s_full + 8 * hb, (j / kSBuf) & 1);
+            tc_after();""", """            { long long c = clock64(); ph_rest += c - c_prev; c_prev = c; }
+            mbar_wait(s_full + 8 * hb, (j / kSBuf) & 1);
+            tc_after();
+            { long long c = clock64(); ph_w += c - c_prev; c_prev = c; }""", 1)
+    s = s.replace("""            for (int hh = 0; hh < kC; ++hh) tc_ld32(s_t + b * kTcKeys + 32 * hh, sr[hh]);
+            tc_wait_ld();""", """            for (int hh = 0; hh < kC; ++hh) tc_ld32(s_t + b * kTcKeys + 32 * hh, sr[hh]);
+            tc_wait_ld();
+            { long long c = clock64(); ph_ld += c - c_prev; c_prev = c; }""", 1)
+    s = s.replace("""            const float mx = fmax3(fmaxf(mxs[0], mxs[1]), mxs[2], mxs[3]) * scale;""", """            const float mx = fmax3(fmaxf(mxs[0], mxs[1]), mxs[2], mxs[3]) * scale;
+            { long long c = clock64() + (mx == 12345.f ? 1 : 0); ph_mx += c - c_prev; c_prev = c; }""", 1)
+    s = s.replace("""            tc_wait_st();
+            float ls[4];""", """            tc_wait_st();
+            { long long c = clock64(); ph_ex += c - c_prev; c_prev = c; }
+            float ls[4];""", 1)
+    s = s.replace("""        // ---- epilogue: O / l (or the split partial) ----""", """        if ((threadIdx.x & 127) == 0) {
+            long long *q = dbgp + 8 * gridDim.x + blockIdx.x * 16 + h * 8;
+            q[0] = ph_w; q[1] = ph_ld; q[2] = ph_mx; q[3] = ph_ex; q[4] = ph_rest; q[5] = nb;
+        }
+        // ---- epilogue: O / l (or the split partial) ----""", 1)
+    assert s.count("ph_ex") == 3, s.count("ph_ex")
 if "nosoftmax" in mode:
     old = '''            uint32_t sr[2][32];
             tc_ld32(s_t + b * kTcKeys, sr[0]);'''

@@ -22,6 +22,11 @@ print("launch ms", s.elapsed_time(e))
 n = L.n_tiles
 d = L.part_lse.view(torch.int64)[1000000:1000000 + n * 8].view(n, 8).cpu().numpy()
 np.save("gpurun_out/qload.npy", d)
+e = L.part_lse.view(torch.int64)[1000000 + n * 8:1000000 + n * 8 + n * 16].view(n, 2, 8).cpu().numpy()
+if e[:, :, 5].any():
+    nbk = np.maximum(e[:, :, 5], 1)
+    for i, nm in enumerate(("wait S", "tcgen05.ld", "max", "exp+P store", "rest (rescale, arrive)")):
+        print(f"softmax per block {nm:24s} half0 {np.median(e[:, 0, i] / nbk[:, 0]):7.0f}  half1 {np.median(e[:, 1, i] / nbk[:, 1]):7.0f} cycles")
 t0 = d[:, 0].min()
 st_, mma0, mma1, end, sm, nb = [d[:, i] for i in range(6)]
 cyc = nb >> 16; nb = nb & 0xffff
