@@ -80,56 +80,64 @@ class StepPlan:
         e_row = np.concatenate([[0], np.cumsum(e_len)[:-1]]).astype(np.int64) if E.size \
             else np.zeros(0, np.int64)
         d_row = Tp + np.arange(D.shape[0], dtype=np.int64)
-        tok_seq, tok_pos, tok_src, kv_seg = [], [], [], [0]
-        dec = {k: [] for k in ("seq", "len", "qoff", "ooff")}
-        dec_seg = [0]
+        # every (layer, slot, entry) at once: item index -1 = replicated
+        # head whose request is routed elsewhere; np.nonzero keeps the
+        # layer-major, slot, entry order of the per-layer tables
+        IDX = eng.item_index_all                             # [L, S, requests]
+        z = np.zeros(0, np.int64)
+        if E.size:
+            itE = IDX[:, :, e_req]
+            l_p, j_p, e_p = np.nonzero(itE >= 0)
+            p_seq, p_st, p_ln, p_row = itE[l_p, j_p, e_p], e_st[e_p], e_len[e_p], e_row[e_p]
+            p_qoff, p_ooff = p_row * rw + j_p * qpk * hd, p_row * ow + j_p * qpk * hd
+            rep = np.repeat(np.arange(p_seq.size), p_ln)
+            local = np.arange(rep.size) - np.repeat(np.cumsum(p_ln) - p_ln, p_ln)
+            tp_seq, tp_pos = p_seq[rep], p_st[rep] + local
+            tp_src, tp_l = (p_row[rep] + local) * rpt + j_p[rep], l_p[rep]
+        else:
+            l_p = p_seq = p_st = p_ln = p_qoff = p_ooff = z
+            tp_seq = tp_pos = tp_src = tp_l = z
+        if D.size:
+            itD = IDX[:, :, d_req]
+            l_d, j_d, k_d = np.nonzero(itD >= 0)
+            dd_seq, dd_len = itD[l_d, j_d, k_d], d_pos[k_d] + 1
+            dd_qoff, dd_ooff = d_row[k_d] * rw + j_d * qpk * hd, d_row[k_d] * ow + j_d * qpk * hd
+            td_pos, td_src = d_pos[k_d], d_row[k_d] * rpt + j_d
+        else:
+            l_d = dd_seq = dd_len = dd_qoff = dd_ooff = td_pos = td_src = z
+        # per-layer segments; the K/V tokens of a layer are its prefill
+        # tokens then its decode tokens (the append is order-free)
+        lay = np.arange(L + 1)
+        p_cut = np.searchsorted(l_p, lay)                    # entries per layer
+        tp_cut = np.searchsorted(tp_l, lay)
+        d_cut = np.searchsorted(l_d, lay)
+        n_tp, n_td = np.diff(tp_cut), np.diff(d_cut)
+        kv_cut = np.concatenate([[0], np.cumsum(n_tp + n_td)])
+        n_kv, n_dec = int(kv_cut[-1]), int(d_cut[-1])
+        tok = np.empty((3, n_kv), dtype=np.int64)
+        pos_p = kv_cut[tp_l] + (np.arange(tp_l.size) - tp_cut[tp_l])
+        pos_d = kv_cut[l_d] + n_tp[l_d] + (np.arange(l_d.size) - d_cut[l_d])
+        tok[:, pos_p] = np.stack([tp_seq, tp_pos, tp_src])
+        tok[:, pos_d] = np.stack([dd_seq, td_pos, td_src])
+        kv_seg = [int(x) for x in kv_cut]
+        dec_seg = [int(x) for x in d_cut]
         self.prefill = []
         tile_plans = {}
         target = default_target_units(eng.cache.dev_index)
-        n_kv = n_dec = 0
         for layer in range(L):
-            idx = eng.item_index[layer]
-            pf = {k: [] for k in ("seq", "start", "len", "qoff", "ooff")}
-            for j in range(len(eng.work.slot_heads[layer])):
-                if E.size:
-                    it = idx[j, e_req]
-                    m = it >= 0  # replicated head: only requests routed here
-                    seq, st, ln, row = it[m], e_st[m], e_len[m], e_row[m]
-                    pf["seq"].append(seq)
-                    pf["start"].append(st)
-                    pf["len"].append(ln)
-                    pf["qoff"].append(row * rw + j * qpk * hd)
-                    pf["ooff"].append(row * ow + j * qpk * hd)
-                    rep = np.repeat(np.arange(seq.size), ln)
-                    local = np.arange(rep.size) - np.repeat(np.cumsum(ln) - ln, ln)
-                    tok_seq.append(seq[rep])
-                    tok_pos.append(st[rep] + local)
-                    tok_src.append((row[rep] + local) * rpt + j)
-                    n_kv += rep.size
-                if D.size:
-                    it = idx[j, d_req]
-                    m = it >= 0
-                    dec["seq"].append(it[m])
-                    dec["len"].append(d_pos[m] + 1)
-                    dec["qoff"].append(d_row[m] * rw + j * qpk * hd)
-                    dec["ooff"].append(d_row[m] * ow + j * qpk * hd)
-                    tok_seq.append(it[m])
-                    tok_pos.append(d_pos[m])
-                    tok_src.append(d_row[m] * rpt + j)
-                    n_kv += int(m.sum())
-                    n_dec += int(m.sum())
-            kv_seg.append(n_kv)
-            dec_seg.append(n_dec)
+            a_, b_ = int(p_cut[layer]), int(p_cut[layer + 1])
             launch = None
-            if pf["seq"] and sum(a.size for a in pf["seq"]):
-                cols = {k: np.concatenate(v) for k, v in pf.items()}
-                key = (cols["start"].tobytes(), cols["len"].tobytes())
+            if b_ > a_ and int(p_ln[a_:b_].sum()):
+                st_, ln_ = p_st[a_:b_], p_ln[a_:b_]
+                key = (st_.tobytes(), ln_.tobytes())
                 tp = tile_plans.get(key)
                 if tp is None:
-                    tp = tile_plans[key] = PrefillTilePlan(cols["start"], cols["len"], qpk, target)
-                launch = PrefillLaunch(eng.cache, cols["seq"], cols["start"], cols["len"],
-                                       cols["qoff"], cols["ooff"], tile_plan=tp, upload=False)
+                    tp = tile_plans[key] = PrefillTilePlan(st_, ln_, qpk, target)
+                launch = PrefillLaunch(eng.cache, p_seq[a_:b_], st_, ln_, p_qoff[a_:b_],
+                                       p_ooff[a_:b_], tile_plan=tp, upload=False)
             self.prefill.append(launch)
+        tok_seq, tok_pos, tok_src = [tok[0]], [tok[1]], [tok[2]]
+        dec = {"seq": [dd_seq], "len": [dd_len], "qoff": [dd_qoff], "ooff": [dd_ooff]}
         cat = (lambda xs: np.concatenate(xs).astype(np.int32) if xs else np.zeros(0, np.int32))
         self.kv_seg = kv_seg
         self.dec_seg = np.array(dec_seg, dtype=np.int32)
@@ -258,6 +266,7 @@ class HybridServingRank(HybridDecodeRank):
             a, b = int(w.seg_items[layer]), int(w.seg_items[layer + 1])
             idx[w.item_slot[a:b], w.item_req[a:b]] = np.arange(a, b)
             self.item_index.append(idx)
+        self.item_index_all = np.stack(self.item_index)  # [L, S, requests]
 
     def plan(self, batch: StepBatch) -> StepPlan:
         return StepPlan(self, batch)
