@@ -49,7 +49,13 @@ struct DecodeParams {
     void *out;
     float *part_o, *part_lse;
     int64_t n_warps;  // W of the stream-K partition
+    int32_t tab_cache;  // decode_cta_kernel: page_off / item_seq staged in smem (n_items <= kTabItems)
 };
+
+// items whose page offsets and block-table rows decode_cta_kernel stages in
+// shared memory at launch (one load round trip instead of the dependent
+// P -> search -> item -> block-table chain before the first page copy)
+constexpr int kTabItems = 1024;
 
 __device__ __forceinline__ int64_t owner_warp(int64_t x, int64_t W, int64_t P) {
     return ((x + 1) * W + P - 1) / P - 1;
@@ -496,6 +502,12 @@ static int launch_decode(const DecodeParams &prm, int sms, cudaStream_t st) {
     size_t smem = (size_t)WARPS * STAGES * (kPageBytes + 8);
     if (KIND == 1)
         smem += (size_t)WARPS * (2 * FS_MAX_Q_PER_KV + FS_MAX_Q_PER_KV * kMergeStride) * 4;
+    // the item-table stage (decode_cta_kernel) when it fits next to the
+    // ring and the merge area; the smem size is fixed per kernel either way
+    const bool tab_fits = KIND == 1 && smem + (size_t)(2 * kTabItems + 1) * 4 <= 227 * 1024;
+    if (tab_fits) smem += (size_t)(2 * kTabItems + 1) * 4;
+    DecodeParams prm2 = prm;
+    prm2.tab_cache = tab_fits && prm.n_items <= kTabItems;
     static bool attr_set[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -517,7 +529,7 @@ static int launch_decode(const DecodeParams &prm, int sms, cudaStream_t st) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = attr;
     lc.numAttrs = 1;
-    FS_CUDA(cudaLaunchKernelEx(&lc, fn, prm));
+    FS_CUDA(cudaLaunchKernelEx(&lc, fn, prm2));
     return cuda_status(cudaGetLastError(), "decode_kernel launch");
 }
 

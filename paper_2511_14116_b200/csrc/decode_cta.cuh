@@ -27,7 +27,23 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_cta_kernel(const DecodeP
     const int gid = lane >> 2, tig = lane & 3;
     constexpr int NT = WARPS * 32;
 
-    const int64_t P = p.page_off[p.n_items];
+    // page offsets + block-table rows of all items -> smem in one round
+    // trip (the first page copy then waits for one dependent load, the
+    // block-table entry, instead of P -> search -> walk -> row -> entry)
+    int32_t *tab = reinterpret_cast<int32_t *>(smem + WARPS * STAGES * (kPageBytes + 8) +
+                                               WARPS * (2 * FS_MAX_Q_PER_KV + FS_MAX_Q_PER_KV * kMergeStride) * 4);
+    const int32_t *off = p.page_off, *iseq = p.item_seq;
+    if (p.tab_cache) {
+        const int n = p.n_items;
+        for (int i = threadIdx.x; i <= n; i += NT) {
+            tab[i] = p.page_off[i];
+            if (i < n) tab[kTabItems + 1 + i] = p.item_seq[i];
+        }
+        __syncthreads();
+        off = tab;
+        iseq = tab + kTabItems + 1;
+    }
+    const int64_t P = off[p.n_items];
     const int64_t C = p.n_warps;  // partition units = CTAs
     const int64_t c = blockIdx.x;
     const int64_t x0 = c * P / C, x1 = (c + 1) * P / C;
@@ -48,7 +64,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_cta_kernel(const DecodeP
     }
     __syncwarp();
 
-    const int32_t *off = p.page_off;
     const int first = find_item(off, p.n_items, x0, lane);
     const int64_t span = x1 - x0;
     const int64_t n_my = span > warp ? (span - warp + WARPS - 1) / WARPS : 0;
@@ -65,7 +80,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_cta_kernel(const DecodeP
         if (j < n_my) {
             const int64_t y = page_of(j);
             while (y >= off[it + 1]) ++it;
-            pg = p.bt[(int64_t)p.item_seq[it] * p.bt_stride + (y - off[it])];
+            pg = p.bt[(int64_t)iseq[it] * p.bt_stride + (y - off[it])];
         }
         wit = max(wit, __shfl_sync(0xffffffffu, it, 31));
         return pg;
