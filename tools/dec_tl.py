@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2511_14116_b200.kvcache import PagedKVCache, RankWork
 from oracle.placement import owner_table
-world, layers, heads, qpk, batch, ctx = 8, 80, 8, 8, 64, 4096
+world, layers, heads, qpk, batch, ctx = [int(v) for v in os.environ.get("DEC_SHAPE", "8,80,8,8,64,4096").split(",")]
 owner = np.array(owner_table("hybrid", layers, heads, range(world)), dtype=np.int32)
 work = RankWork.build(owner, 0, {r: r % world for r in range(batch)}, batch)
 cache = PagedKVCache(work, ctx, qpk)
