@@ -404,20 +404,30 @@ __global__ void __launch_bounds__(kTileM) gemm_reduce_kernel(const GemmParams p,
     float g[kRedRows], uu[kRedRows];
 #pragma unroll
     for (int r = 0; r < kRedRows; ++r) g[r] = uu[r] = 0.f;
-    for (int64_t s = clo; s <= chi; ++s) {  // CTA order
-        if (U < C && !gemm_live(s, C, U)) continue;
-        const float *src = p.ws + (t + s) * (kRowsN * kTileM) + r0 * kTileM + m;
-        float vg[kRedRows], vu[kRedRows];
+    // 4 contributors' rows in flight per round (a split tile of a small GEMM
+    // has up to ~15 contributors; one round trip per contributor was the
+    // whole cost), summed in CTA order
+    const bool all_live = U >= C;
+    for (int64_t s0 = clo; s0 <= chi; s0 += 4) {
+        float vg[4][kRedRows], vu[4][kRedRows];
 #pragma unroll
-        for (int r = 0; r < kRedRows; ++r) {
-            vg[r] = __ldcg(src + r * kTileM);
-            vu[r] = swiglu ? __ldcg(src + r * kTileM + 64) : 0.f;
+        for (int i = 0; i < 4; ++i) {
+            const int64_t s = s0 + i;
+            const bool ok = s <= chi && (all_live || gemm_live(s, C, U));
+            const float *src = p.ws + (t + (ok ? s : clo)) * (kRowsN * kTileM) + r0 * kTileM + m;
+#pragma unroll
+            for (int r = 0; r < kRedRows; ++r) {
+                vg[i][r] = ok ? __ldcg(src + r * kTileM) : 0.f;
+                vu[i][r] = ok && swiglu ? __ldcg(src + r * kTileM + 64) : 0.f;
+            }
         }
 #pragma unroll
-        for (int r = 0; r < kRedRows; ++r) {
-            g[r] += vg[r];
-            uu[r] += vu[r];
-        }
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int r = 0; r < kRedRows; ++r) {
+                g[r] += vg[i][r];
+                uu[r] += vu[i][r];
+            }
     }
 #pragma unroll
     for (int r = 0; r < kRedRows; ++r) {
