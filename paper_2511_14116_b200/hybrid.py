@@ -317,10 +317,11 @@ class HybridDecodeRank:
     def launches_per_step(self) -> int:
         """Our kernel launches per step: the fused decode launch per layer,
         plus the swiglu launch per layer with the MLP (cuBLAS GEMMs), or the
-        decode + 4 tcgen05 GEMM launches per layer (gemm="tcgen05")."""
+        decode + 4 tcgen05 GEMMs per layer, each a GEMM launch and its
+        split-tile reduction launch (gemm="tcgen05")."""
         has_mlp = self.mlp and len(self.ffn_cols)
         if self.gemm == "tcgen05":
-            return self.model.num_layers * (5 if has_mlp else 3)
+            return self.model.num_layers * (1 + 2 * (4 if has_mlp else 2))
         n = self.model.num_layers * (2 if has_mlp else 1)
         if self.xchg is not None:  # one fs_ar_residual per exchange
             n += self.model.num_layers * (2 if self.mlp else 1)
