@@ -258,9 +258,12 @@ int fs_pages_scatter(void *kv_pool, const int32_t *page_ids, int32_t n_pages,
  * x: bf16 [rows <= 64][K] (row stride ld_x), W: bf16 [K][N] (row stride ld_w,
  * w_layout 0) or packed in 128-column panels [N/128][K][128] (w_layout 1:
  * every 64 x 128 slice the kernel streams is one contiguous 16 KB block),
- * K % 64 == 0, N % 128 == 0.  workspace: >= fs_gemm_workspace_floats fp32;
- * sems: 2*N/128 int32, zero-initialised (left zero).  Launched with
- * programmatic dependent launch (W prefetch overlaps the previous kernel). */
+ * K % 64 == 0, N % 128 == 0.  workspace: >= fs_gemm_workspace_floats fp32
+ * (the fp32 partials of split tiles); sems: 2*N/128 int32 (reserved: the
+ * split tiles are summed by a second, PDL-launched kernel, so no in-grid
+ * semaphores are used; must be non-null).  Two launches on `stream`: the
+ * GEMM (programmatic dependent launch: W prefetch overlaps the previous
+ * kernel) and the split-tile reduction. */
 int64_t fs_gemm_workspace_floats(int device, int32_t N, int32_t epilogue);
 int fs_gemm_skinny(const void *x, int64_t ld_x, int32_t rows, int32_t K, const void *w,
                    int64_t ld_w, int32_t w_layout, int32_t N, void *out, int64_t ld_out, const void *res,

@@ -10,8 +10,9 @@
 // evenly, so skinny shapes with few column tiles (Llama-70B qkv at 8 GPUs:
 // 10 tiles) still use every SM and every byte of W is read exactly once.  A
 // CTA that covers a whole tile applies the epilogue directly; otherwise it
-// writes an fp32 partial to slot `tile + cta`, and the tile's last
-// contributor (semaphore) sums the partials in CTA order (deterministic).
+// writes an fp32 partial to slot `tile + cta`, and gemm_reduce_kernel (the
+// next launch, PDL) sums each split tile's partials in CTA order
+// (deterministic) and applies the epilogue.
 //
 // Roles (192 threads): warp 4 = TMA producer, warp 5 = MMA issuer, warps 0-3
 // = epilogue (TMEM lane quadrant = warp index).  Fused epilogues: plain
@@ -56,7 +57,7 @@ struct GemmParams {
     const __nv_bfloat16 *res;
     int64_t ld_res;
     float *ws;          // partial slots, each [64][128] fp32
-    int32_t *sems;      // per tile, zero-initialised, left zero
+    int32_t *sems;      // reserved (ABI): split tiles are reduced by gemm_reduce_kernel
     unsigned long long *dbg;  // optional per-CTA phase timestamps (ns)
 };
 
