@@ -435,3 +435,29 @@ def test_decode_long_context_per_item_tolerance(qpk):
             row = r * work.n_slots + j
             k, v = kv[i]
             _close(got[row], head_decode(qn[row], k[:lens[r]], v[:lens[r]], 1 / math.sqrt(128)))
+
+
+@pytest.mark.parametrize("n_req", [1024, 1100])
+def test_decode_many_items_table_stage_boundary(n_req):
+    """decode_cta_kernel stages the item tables in shared memory for up to
+    1024 items per launch and reads them from global memory beyond that:
+    both sides of the boundary (one TP head, ragged short contexts) match
+    the oracle."""
+    from oracle.attention import head_decode
+    owner = np.zeros((1, 1), dtype=np.int32)  # one layer, one KV head, rank 0
+    rng = np.random.default_rng(n_req)
+    lens = [int(x) for x in rng.integers(1, 70, size=n_req)]
+    routing = {r: 0 for r in range(n_req)}
+    qpk = 4
+    gen = torch.Generator().manual_seed(n_req)
+    work, cache = _build(owner, 0, routing, lens, qpk, config=0)
+    assert work.n_items == n_req
+    kv = _fill(cache, work, lens, gen)
+    q = _bf16(torch.randn((n_req, qpk, 128), generator=gen))
+    out = torch.zeros((n_req, qpk, 128), dtype=torch.float32, device="cuda")
+    cache.decode_layer(0, q.cuda(), out)
+    torch.cuda.synchronize()
+    qn = q.double().numpy()
+    exp = np.stack([head_decode(qn[i], kv[i][0][:lens[i]], kv[i][1][:lens[i]], 1 / math.sqrt(128))
+                    for i in range(n_req)])
+    _close(out.cpu().numpy(), exp)
