@@ -16,11 +16,12 @@ ap.add_argument("--ctx", type=int, default=4096)
 ap.add_argument("--configs", default="0,1,2,3,7")
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--graph", action="store_true")
+ap.add_argument("--order", default="contiguous", help="page order: contiguous | shuffled | interleaved")
 a = ap.parse_args()
 owner = np.array(owner_table("hybrid", a.layers, a.heads, range(a.world)), dtype=np.int32)
 routing = {r: r % a.world for r in range(a.batch)}
 work = RankWork.build(owner, a.rank, routing, a.batch)
-cache = PagedKVCache(work, a.ctx, a.qpk)
+cache = PagedKVCache(work, a.ctx, a.qpk, page_order=a.order)
 cache.pool.view(torch.bfloat16).normal_()
 cache.set_lengths([a.ctx] * a.batch)
 rows = a.batch * work.n_slots
