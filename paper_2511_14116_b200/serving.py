@@ -321,6 +321,20 @@ class HybridServingRank(HybridDecodeRank):
             xs.copy_(x, non_blocking=True)
         if self.xchg is not None:
             return self._serve_fused(plan, xs)
+        if self.group is None:
+            # no exchange: the residual add rides on the projection GEMMs
+            # (cuBLAS beta = 1) instead of a separate elementwise pass
+            has_ffn = self.mlp and len(self.ffn_cols)
+            C = len(self.ffn_cols)
+            for layer in range(self.model.num_layers):
+                self._attention(layer, plan)
+                xs.addmm_(self.o_s[:T], self.wo[layer])
+                if has_ffn:
+                    torch.matmul(xs, self.w_gu[layer], out=self.h_s[:T])
+                    N.check(N.lib.fs_swiglu(N.ptr(self.h_s), T, C, 2 * C, N.ptr(self.act_s), C,
+                                            _stream()), "fs_swiglu")
+                    xs.addmm_(self.act_s[:T], self.w_d[layer])
+            return xs
         for layer in range(self.model.num_layers):
             part = self.serve_attention_partial(layer, plan)
             if self.group is not None:
