@@ -231,6 +231,18 @@ int fs_kv_write(void *kv_pool, const int32_t *block_table, int64_t bt_stride,
                 const int32_t *tok_src, int32_t n_tok, const void *k_src,
                 const void *v_src, int64_t src_stride, void *stream);
 
+/* K3 over runs of consecutive tokens (the serving iteration's form: one
+ * run per (prefill chunk or decode token, head slot)): run r covers tokens
+ * run_off[r] - run_off[0] .. run_off[r+1] - run_off[0] - 1 of this launch;
+ * its i-th token goes to sequence run_seq[r] at position run_pos[r] + i and
+ * its K/V are rows run_src[r] + i * src_step of k_src / v_src.  run_off:
+ * n_runs + 1 nondecreasing entries (a slice of a prefix sum is fine);
+ * n_tok = run_off[n_runs] - run_off[0] (the host's copy: sizes the grid). */
+int fs_kv_write_runs(void *kv_pool, const int32_t *block_table, int64_t bt_stride,
+                     const int32_t *run_seq, const int32_t *run_pos, const int32_t *run_src,
+                     const int32_t *run_off, int32_t n_runs, int32_t n_tok, int32_t src_step,
+                     const void *k_src, const void *v_src, int64_t src_stride, void *stream);
+
 /* inverse of fs_kv_write (tests / debugging) */
 int fs_kv_read(const void *kv_pool, const int32_t *block_table, int64_t bt_stride,
                const int32_t *tok_seq, const int32_t *tok_pos,

@@ -29,6 +29,33 @@ __global__ void __launch_bounds__(256) kv_write_kernel(uint8_t *pool, const int3
     *reinterpret_cast<uint4 *>(dst) = half ? bf16x8_to_f16x8(v) : v;  // V pages hold f16
 }
 
+// K3 over token runs: warp = token; the run is found by a binary search of
+// the run prefix (a few hundred runs per layer)
+__global__ void __launch_bounds__(256) kv_write_runs_kernel(
+    uint8_t *pool, const int32_t *bt, int64_t bt_stride, const int32_t *run_seq,
+    const int32_t *run_pos, const int32_t *run_src, const int32_t *run_off, int32_t n_runs,
+    int32_t src_step, const uint8_t *k_src, const uint8_t *v_src, int64_t src_stride_bytes) {
+    const int32_t base = run_off[0];
+    const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= (int64_t)run_off[n_runs] - base) return;
+    int lo = 0, hi = n_runs;  // run_off[lo] - base <= t < run_off[hi] - base
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (run_off[mid] - base <= t) lo = mid;
+        else hi = mid;
+    }
+    const int32_t i = (int32_t)(t - (run_off[lo] - base));
+    const int32_t pos = run_pos[lo] + i;
+    const int64_t page = bt[(int64_t)run_seq[lo] * bt_stride + pos / kPageTokens];
+    const uint32_t r = pos % kPageTokens, c = lane & 15, half = lane >> 4;
+    const uint8_t *src = (half ? v_src : k_src) +
+                         ((int64_t)run_src[lo] + (int64_t)i * src_step) * src_stride_bytes + c * 16;
+    uint8_t *dst = pool + page * kPageBytes + half * kHalfPage + swz(r, c);
+    const uint4 v = *reinterpret_cast<const uint4 *>(src);
+    *reinterpret_cast<uint4 *>(dst) = half ? bf16x8_to_f16x8(v) : v;  // V pages hold f16
+}
+
 __global__ void __launch_bounds__(256) kv_read_kernel(const uint8_t *pool, const int32_t *bt,
                                                       int64_t bt_stride, const int32_t *tok_seq,
                                                       const int32_t *tok_pos,
@@ -98,6 +125,26 @@ extern "C" int fs_kv_write(void *kv_pool, const int32_t *block_table, int64_t bt
         static_cast<uint8_t *>(kv_pool), block_table, bt_stride, tok_seq, tok_pos, tok_src, n_tok,
         static_cast<const uint8_t *>(k_src), static_cast<const uint8_t *>(v_src), src_stride * 2);
     return cuda_status(cudaGetLastError(), "kv_write_kernel launch");
+}
+
+extern "C" int fs_kv_write_runs(void *kv_pool, const int32_t *block_table, int64_t bt_stride,
+                                const int32_t *run_seq, const int32_t *run_pos,
+                                const int32_t *run_src, const int32_t *run_off, int32_t n_runs,
+                                int32_t n_tok, int32_t src_step, const void *k_src,
+                                const void *v_src, int64_t src_stride, void *stream) {
+    FS_CHECK_ARG(n_runs >= 0 && n_tok >= 0, "n_runs and n_tok must be nonnegative");
+    if (n_runs == 0 || n_tok == 0) return FS_OK;
+    FS_CHECK_ARG(kv_pool && block_table && run_seq && run_pos && run_src && run_off && k_src &&
+                     v_src, "null pointer");
+    FS_CHECK_ARG(src_stride % 8 == 0 && src_stride >= kHeadDim,
+                 "src_stride must be a multiple of 8 and >= %d", kHeadDim);
+    const int64_t threads = (int64_t)n_tok * 32;
+    kv_write_runs_kernel<<<(unsigned)((threads + 255) / 256), 256, 0,
+                           static_cast<cudaStream_t>(stream)>>>(
+        static_cast<uint8_t *>(kv_pool), block_table, bt_stride, run_seq, run_pos, run_src, run_off,
+        n_runs, src_step, static_cast<const uint8_t *>(k_src), static_cast<const uint8_t *>(v_src),
+        src_stride * 2);
+    return cuda_status(cudaGetLastError(), "kv_write_runs_kernel launch");
 }
 
 extern "C" int fs_kv_read(const void *kv_pool, const int32_t *block_table, int64_t bt_stride,

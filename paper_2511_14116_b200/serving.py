@@ -90,13 +90,9 @@ class StepPlan:
             l_p, j_p, e_p = np.nonzero(itE >= 0)
             p_seq, p_st, p_ln, p_row = itE[l_p, j_p, e_p], e_st[e_p], e_len[e_p], e_row[e_p]
             p_qoff, p_ooff = p_row * rw + j_p * qpk * hd, p_row * ow + j_p * qpk * hd
-            rep = np.repeat(np.arange(p_seq.size), p_ln)
-            local = np.arange(rep.size) - np.repeat(np.cumsum(p_ln) - p_ln, p_ln)
-            tp_seq, tp_pos = p_seq[rep], p_st[rep] + local
-            tp_src, tp_l = (p_row[rep] + local) * rpt + j_p[rep], l_p[rep]
+            p_src = p_row * rpt + j_p                        # K/V row of the run's first token
         else:
-            l_p = p_seq = p_st = p_ln = p_qoff = p_ooff = z
-            tp_seq = tp_pos = tp_src = tp_l = z
+            l_p = p_seq = p_st = p_ln = p_qoff = p_ooff = p_src = z
         if D.size:
             itD = IDX[:, :, d_req]
             l_d, j_d, k_d = np.nonzero(itD >= 0)
@@ -105,21 +101,24 @@ class StepPlan:
             td_pos, td_src = d_pos[k_d], d_row[k_d] * rpt + j_d
         else:
             l_d = dd_seq = dd_len = dd_qoff = dd_ooff = td_pos = td_src = z
-        # per-layer segments; the K/V tokens of a layer are its prefill
-        # tokens then its decode tokens (the append is order-free)
+        # K3 runs (consecutive tokens of one entry and head slot) per layer:
+        # its prefill runs, then its decode tokens (runs of 1); the device
+        # expands them (fs_kv_write_runs), the host never lists tokens
         lay = np.arange(L + 1)
-        p_cut = np.searchsorted(l_p, lay)                    # entries per layer
-        tp_cut = np.searchsorted(tp_l, lay)
+        p_cut = np.searchsorted(l_p, lay)                    # prefill runs per layer
         d_cut = np.searchsorted(l_d, lay)
-        n_tp, n_td = np.diff(tp_cut), np.diff(d_cut)
-        kv_cut = np.concatenate([[0], np.cumsum(n_tp + n_td)])
-        n_kv, n_dec = int(kv_cut[-1]), int(d_cut[-1])
-        tok = np.empty((3, n_kv), dtype=np.int64)
-        pos_p = kv_cut[tp_l] + (np.arange(tp_l.size) - tp_cut[tp_l])
-        pos_d = kv_cut[l_d] + n_tp[l_d] + (np.arange(l_d.size) - d_cut[l_d])
-        tok[:, pos_p] = np.stack([tp_seq, tp_pos, tp_src])
-        tok[:, pos_d] = np.stack([dd_seq, td_pos, td_src])
-        kv_seg = [int(x) for x in kv_cut]
+        n_pr, n_dr = np.diff(p_cut), np.diff(d_cut)
+        run_cut = np.concatenate([[0], np.cumsum(n_pr + n_dr)])
+        n_run, n_dec = int(run_cut[-1]), int(d_cut[-1])
+        runs = np.empty((4, n_run), dtype=np.int64)          # seq, pos, src, len
+        pos_p = run_cut[l_p] + (np.arange(l_p.size) - p_cut[l_p])
+        pos_d = run_cut[l_d] + n_pr[l_d] + (np.arange(l_d.size) - d_cut[l_d])
+        runs[:, pos_p] = np.stack([p_seq, p_st, p_src, p_ln])
+        runs[:, pos_d] = np.stack([dd_seq, td_pos, td_src, np.ones_like(dd_seq)])
+        run_off = np.concatenate([[0], np.cumsum(runs[3])])
+        kv_seg = [int(x) for x in run_cut]
+        self.kv_tokens = [int(run_off[run_cut[l + 1]] - run_off[run_cut[l]]) for l in range(L)]
+        self.src_step = rpt
         dec_seg = [int(x) for x in d_cut]
         self.prefill = []
         tile_plans = {}
@@ -136,13 +135,13 @@ class StepPlan:
                 launch = PrefillLaunch(eng.cache, p_seq[a_:b_], st_, ln_, p_qoff[a_:b_],
                                        p_ooff[a_:b_], tile_plan=tp, upload=False)
             self.prefill.append(launch)
-        tok_seq, tok_pos, tok_src = [tok[0]], [tok[1]], [tok[2]]
         dec = {"seq": [dd_seq], "len": [dd_len], "qoff": [dd_qoff], "ooff": [dd_ooff]}
         cat = (lambda xs: np.concatenate(xs).astype(np.int32) if xs else np.zeros(0, np.int32))
         self.kv_seg = kv_seg
         self.dec_seg = np.array(dec_seg, dtype=np.int32)
         d_len = cat(dec["len"])
-        parts = [cat(tok_seq), cat(tok_pos), cat(tok_src), cat(dec["seq"]), d_len,
+        parts = [runs[0].astype(np.int32), runs[1].astype(np.int32), runs[2].astype(np.int32),
+                 run_off.astype(np.int32), cat(dec["seq"]), d_len,
                  cat(dec["qoff"]), cat(dec["ooff"]), self.dec_seg]
         pf_base = sum(x.size for x in parts)
         for lp in self.prefill:
@@ -152,8 +151,8 @@ class StepPlan:
         self._tab = torch.from_numpy(np.concatenate(parts)).to(dev)
         o = 0
         self._off = {}
-        for name, size in (("tok_seq", n_kv), ("tok_pos", n_kv), ("tok_src", n_kv),
-                           ("d_seq", n_dec), ("d_len", n_dec), ("d_qoff", n_dec),
+        for name, size in (("run_seq", n_run), ("run_pos", n_run), ("run_src", n_run),
+                           ("run_off", n_run + 1), ("d_seq", n_dec), ("d_len", n_dec), ("d_qoff", n_dec),
                            ("d_ooff", n_dec), ("d_seg", L + 1)):
             self._off[name] = o
             o += size
@@ -280,12 +279,13 @@ class HybridServingRank(HybridDecodeRank):
         if b > a:                                                        # K3
             hd = self.model.head_dim
             qw = self.n_slots * self.qpk * hd
-            N.check(N.lib.fs_kv_write(
+            N.check(N.lib.fs_kv_write_runs(
                 N.ptr(self.cache.pool), N.ptr(self.cache.block_table), self.cache.pages_per_seq,
-                plan.ptr("tok_seq", a), plan.ptr("tok_pos", a), plan.ptr("tok_src", a), b - a,
+                plan.ptr("run_seq", a), plan.ptr("run_pos", a), plan.ptr("run_src", a),
+                plan.ptr("run_off", a), b - a, plan.kv_tokens[layer], plan.src_step,
                 N.C.c_void_p(qkv.data_ptr() + 2 * qw),
                 N.C.c_void_p(qkv.data_ptr() + 2 * (qw + self.n_slots * hd)), hd, _stream()),
-                "fs_kv_write")
+                "fs_kv_write_runs")
         o.zero_()  # replicated slots of requests routed elsewhere stay 0
         pf = plan.prefill[layer]
         if pf is not None:                                               # K8
