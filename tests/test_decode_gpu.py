@@ -179,6 +179,50 @@ def test_kv_write_read_roundtrip_bitexact():
             assert torch.equal(raw[c >> 3, r, (c & 7) ^ (r & 7)], k[r, c * 8:(c + 1) * 8])
 
 
+def test_kv_write_runs_matches_token_writes():
+    """fs_kv_write_runs (runs of consecutive tokens, strided source rows, a
+    slice of a prefix sum) leaves the pool bit-identical to fs_kv_write of
+    the same tokens listed one by one."""
+    from paper_2511_14116_b200 import _native as N
+    from paper_2511_14116_b200.kvcache import PagedKVCache, RankWork
+    owner = np.zeros((1, 3), dtype=np.int32)
+    work = RankWork.build(owner, 0, {0: 0, 1: 0}, 2)
+    step, rows = 3, 400  # source rows: run r's token i at run_src[r] + i * step
+    src_k = torch.randn((rows * step, 128), device="cuda").to(torch.bfloat16)
+    src_v = torch.randn((rows * step, 128), device="cuda").to(torch.bfloat16)
+    # runs: (seq, pos0, src0, len); a leading dummy run is skipped via the slice
+    runs = [(0, 0, 0, 1), (1, 5, 1, 37), (3, 0, 2, 1), (4, 17, 40, 100), (2, 99, 9, 1),
+            (5, 0, 300, 16)]
+    seq = np.array([r[0] for r in runs], np.int32)
+    pos = np.array([r[1] for r in runs], np.int32)
+    src = np.array([r[2] for r in runs], np.int32)
+    off = np.concatenate([[7], 7 + np.cumsum([r[3] for r in runs])]).astype(np.int32)
+    t_seq = np.concatenate([[s] * n for s, _, _, n in runs[1:]]).astype(np.int32)
+    t_pos = np.concatenate([np.arange(p, p + n) for _, p, _, n in runs[1:]]).astype(np.int32)
+    t_src = np.concatenate([s + step * np.arange(n) for _, _, s, n in runs[1:]]).astype(np.int32)
+    pools = []
+    for mode in ("runs", "tokens"):
+        cache = PagedKVCache(work, 200, 1, page_order="shuffled", seed=3)
+        st = N.C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        if mode == "runs":
+            dev = [torch.from_numpy(a).cuda() for a in (seq, pos, src, off)]
+            N.check(N.lib.fs_kv_write_runs(
+                N.ptr(cache.pool), N.ptr(cache.block_table), cache.pages_per_seq,
+                N.C.c_void_p(dev[0].data_ptr() + 4), N.C.c_void_p(dev[1].data_ptr() + 4),
+                N.C.c_void_p(dev[2].data_ptr() + 4), N.C.c_void_p(dev[3].data_ptr() + 4),
+                len(runs) - 1, int(off[-1] - off[1]), step, N.ptr(src_k), N.ptr(src_v), 128, st),
+                "fs_kv_write_runs")
+        else:
+            dev = [torch.from_numpy(a).cuda() for a in (t_seq, t_pos, t_src)]
+            N.check(N.lib.fs_kv_write(N.ptr(cache.pool), N.ptr(cache.block_table),
+                                      cache.pages_per_seq, N.ptr(dev[0]), N.ptr(dev[1]),
+                                      N.ptr(dev[2]), t_seq.size, N.ptr(src_k), N.ptr(src_v), 128,
+                                      st), "fs_kv_write")
+        torch.cuda.synchronize()
+        pools.append(cache.pool.clone())
+    assert torch.equal(pools[0], pools[1])
+
+
 def test_plan_pages_matches_host_prefix():
     from paper_2511_14116_b200.kvcache import PagedKVCache, RankWork
     rng = np.random.default_rng(0)
