@@ -266,6 +266,11 @@ class HybridServingRank(HybridDecodeRank):
             idx[w.item_slot[a:b], w.item_req[a:b]] = np.arange(a, b)
             self.item_index.append(idx)
         self.item_index_all = np.stack(self.item_index)  # [L, S, requests]
+        # head slots a layer's kernels do not fill for every request (the
+        # replicated heads: only routed requests): their o columns are zeroed
+        # per iteration, the fully served (TP) slots are not
+        self.partial_slots = [np.nonzero((self.item_index_all[l] < 0).any(axis=1))[0].tolist()
+                              for l in range(model.num_layers)]
 
     def plan(self, batch: StepBatch) -> StepPlan:
         return StepPlan(self, batch)
@@ -286,7 +291,9 @@ class HybridServingRank(HybridDecodeRank):
                 N.C.c_void_p(qkv.data_ptr() + 2 * qw),
                 N.C.c_void_p(qkv.data_ptr() + 2 * (qw + self.n_slots * hd)), hd, _stream()),
                 "fs_kv_write_runs")
-        o.zero_()  # replicated slots of requests routed elsewhere stay 0
+        w = self.qpk * self.model.head_dim
+        for j in self.partial_slots[layer]:  # replicated slots: rows routed elsewhere stay 0
+            o[:, j * w:(j + 1) * w].zero_()
         pf = plan.prefill[layer]
         if pf is not None:                                               # K8
             pf(qkv, self.row_width, o, o.shape[1])
