@@ -193,7 +193,8 @@ typedef struct fs_prefill_desc {
     int32_t n_comb;
     int32_t q_per_kv;          /* 1..8                                      */
     float scale;
-    float *part_o;             /* [partial_slots][rows][128] fp32           */
+    void *part_o;              /* [partial_slots][rows][128] f16 (split
+                                  partials O / l; bounded by max |V|)       */
     float *part_lse;           /* [partial_slots][rows]                     */
     int64_t partial_slots;
     int32_t variant;           /* 0: tcgen05 (TMEM accumulators, 256-row

@@ -55,7 +55,8 @@ struct PrefillParams {
     int32_t qpk, tpt;  // q heads per kv head, chunk tokens per tile
     int32_t rows;      // query rows per tile (= partial rows per slot): 64 or 128
     float scale_log2;
-    float *part_o, *part_lse;
+    __half *part_o;     // split partials O / l: f16 (|O| <= max|V|, f16 V pages)
+    float *part_lse;
 };
 
 template <int STAGES>
@@ -269,12 +270,12 @@ __global__ void __launch_bounds__((kConsumerWarps + 2) * 32) prefill_kernel(cons
             }
         }
     } else {
-        float *po = p.part_o + (int64_t)slot * kTileRows * kHeadDim;
+        __half *po = p.part_o + (int64_t)slot * kTileRows * kHeadDim;
 #pragma unroll
         for (int nt = 0; nt < 16; ++nt) {
             const int d = nt * 8 + 2 * tig;
-            *reinterpret_cast<float2 *>(po + ra * kHeadDim + d) = make_float2(o[nt][0] * ia, o[nt][1] * ia);
-            *reinterpret_cast<float2 *>(po + rb * kHeadDim + d) = make_float2(o[nt][2] * ib, o[nt][3] * ib);
+            *reinterpret_cast<uint32_t *>(po + ra * kHeadDim + d) = pack_f16(o[nt][0] * ia, o[nt][1] * ia);
+            *reinterpret_cast<uint32_t *>(po + rb * kHeadDim + d) = pack_f16(o[nt][2] * ib, o[nt][3] * ib);
         }
         if (tig == 0) {
             p.part_lse[(int64_t)slot * kTileRows + ra] = la > 0.f ? ma + __log2f(la) : -INFINITY;
@@ -313,35 +314,33 @@ __global__ void __launch_bounds__(256) prefill_combine_kernel(const PrefillParam
 #pragma unroll
         for (int i = 0; i < 8; ++i) mx = fmaxf(mx, v[i]);
     }
-    const float4 *po = reinterpret_cast<const float4 *>(p.part_o + ((int64_t)slot0 * p.rows + r) * kHeadDim) + 2 * c;
-    const int64_t sstr = (int64_t)p.rows * (kHeadDim / 4);  // float4s per split slot
+    const uint4 *po = reinterpret_cast<const uint4 *>(p.part_o + ((int64_t)slot0 * p.rows + r) * kHeadDim) + c;
+    const int64_t sstr = (int64_t)p.rows * (kHeadDim / 8);  // 16-B chunks per split slot
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     float den = 0.f;
     for (int s0 = 0; s0 < ns; s0 += 4) {
         float w[4];
-        float4 va[4], vb[4];
+        uint4 vv[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             w[i] = 0.f;
-            va[i] = vb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            vv[i] = make_uint4(0, 0, 0, 0);
             if (s0 + i < ns) {
                 const float l = __ldg(lse + (int64_t)(s0 + i) * p.rows);
                 w[i] = l == -INFINITY ? 0.f : fast_exp2(l - mx);
-                va[i] = __ldg(po + (s0 + i) * sstr);
-                vb[i] = __ldg(po + (s0 + i) * sstr + 1);
+                vv[i] = __ldg(po + (s0 + i) * sstr);
             }
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             den += w[i];
-            acc[0] += w[i] * va[i].x;
-            acc[1] += w[i] * va[i].y;
-            acc[2] += w[i] * va[i].z;
-            acc[3] += w[i] * va[i].w;
-            acc[4] += w[i] * vb[i].x;
-            acc[5] += w[i] * vb[i].y;
-            acc[6] += w[i] * vb[i].z;
-            acc[7] += w[i] * vb[i].w;
+            const uint32_t hw[4] = {vv[i].x, vv[i].y, vv[i].z, vv[i].w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&hw[k]));
+                acc[2 * k] += w[i] * f.x;
+                acc[2 * k + 1] += w[i] * f.y;
+            }
         }
     }
     const float inv = den > 0.f ? 1.f / den : 0.f;
@@ -523,7 +522,7 @@ extern "C" int fs_prefill_attention(const fs_prefill_desc *d, void *stream) {
     prm.rows = variant_rows(d->variant);
     prm.tpt = prm.rows / d->q_per_kv;
     prm.scale_log2 = d->scale * 1.4426950408889634f;
-    prm.part_o = d->part_o;
+    prm.part_o = static_cast<__half *>(d->part_o);
     prm.part_lse = d->part_lse;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     static bool attr_set[4][64] = {{false}};

@@ -540,8 +540,11 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
         for (int rr = 0; rr < 32; ++rr) {
             const float4 v = reinterpret_cast<const float4 *>(stg + rr * kHeadDim)[lane ^ (rr & 7)];
             const int Rr = wrow0 + rr;
-            if (slot >= 0) {
-                reinterpret_cast<float4 *>(p.part_o + ((int64_t)slot * rows + Rr) * kHeadDim)[lane] = v;
+            if (slot >= 0) {  // f16 partial: 4 dims = 8 B per lane
+                uint2 hv;
+                hv.x = pack_f16(v.x, v.y);
+                hv.y = pack_f16(v.z, v.w);
+                reinterpret_cast<uint2 *>(p.part_o + ((int64_t)slot * rows + Rr) * kHeadDim)[lane] = hv;
                 continue;
             }
             const int tk = tok0 + Rr / qpk;
