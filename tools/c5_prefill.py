@@ -13,7 +13,8 @@ T = sum(lens)
 q = torch.randn((T, stride), device="cuda").to(torch.bfloat16)
 out = torch.empty_like(q)
 row0 = np.concatenate([[0], np.cumsum(lens)[:-1]]) * stride
-L = PrefillLaunch(cache, np.arange(cnt), starts, lens, row0, row0)
+variant = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+L = PrefillLaunch(cache, np.arange(cnt), starts, lens, row0, row0, variant=variant)
 for _ in range(5): L(q, stride, out, stride)
 torch.cuda.synchronize()
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -21,4 +22,4 @@ s.record()
 for _ in range(20): L(q, stride, out, stride)
 e.record(); torch.cuda.synchronize()
 ms = s.elapsed_time(e) / 20
-print(f"C5-like chunk: {ms*1e3:.1f} us  {L.flops/ms/1e9:.1f} TFLOP/s tiles {L.n_tiles} comb {L.n_comb}")
+print(f"C5-like chunk v{variant}: {ms*1e3:.1f} us  {L.flops/ms/1e9:.1f} TFLOP/s tiles {L.n_tiles} comb {L.n_comb}")
