@@ -50,7 +50,10 @@ METRIC = ("decode tokens/s at 8→7→6→5 B200 (fraction of HBM roofline); "
 UNIT = "tokens/s"
 KV_UNIT = 512  # bytes per (kv head, token): K+V, head_dim 128, bf16 (core.py:101-103)
 GEMM_BACKEND = "cublas"  # --gemm: projections via cuBLAS or the tcgen05 skinny GEMM
-EXCHANGE = "fused"  # --exchange (N>1): fs_ar_residual over peer memory, or NCCL all-reduce
+EXCHANGE = "fused"
+# fs_decode_attention configs -> the kernel instance that runs (csrc/decode.cu)
+KERNEL_NAMES = {0: "decode_cta_kernel<8,2>", 3: "decode_cta_kernel<16,1>",
+                7: "decode_kernel<4,4,1>", 9: "decode_kernel<8,2,1>"}  # --exchange (N>1): fs_ar_residual over peer memory, or NCCL all-reduce
 
 
 def measured_peaks():
@@ -424,102 +427,68 @@ def cost_calibration(fstates, mixed, batch=64, ctx=4096, fails=(7, 3, 5), budget
 
 
 # ------------------------------------------------------------ CPU oracle --
-def cpu_oracle_rate(qpk, ctx, seconds=8.0):
-    """Items/s of the oracle port (float64 numpy decode of one (kv head,
-    request) item, refexec.py:85-103) on all host cores, one thread per
-    item; returns (items_per_s, cores, items_done)."""
-    import numpy as np
-    from concurrent.futures import ThreadPoolExecutor
-    from oracle.attention import head_decode
-    try:
-        from threadpoolctl import threadpool_limits
-    except Exception:  # pragma: no cover
-        threadpool_limits = None
-    cores = len(os.sched_getaffinity(0))
-    rng = np.random.default_rng(0)
-    k = rng.standard_normal((ctx, 128)).astype(np.float32)
-    v = rng.standard_normal((ctx, 128)).astype(np.float32)
-    qs = [rng.standard_normal((qpk, 128)).astype(np.float32) for _ in range(cores)]
-    scale = 1.0 / np.sqrt(128)
-    done = [0] * cores
-    stop = time.perf_counter() + seconds
+C2_SHAPE = dict(hidden=4096, kv_heads=8, qpk=4, hd=128, ffn=14336, batch=64, ctx=4096, layers=32)
 
-    def worker(i):
-        while time.perf_counter() < stop:
-            head_decode(qs[i], k, v, scale)
-            done[i] += 1
 
-    ctx_mgr = threadpool_limits(1) if threadpool_limits else None
+def cpu_decode_step(layer_samples):
+    """The reference's CPU path for the hot path, like for like with the GPU
+    step: the float64 oracle restatement of one hybrid decode step
+    (oracle/decode_step.py: refexec.py:249-308 decode form -- QKV
+    projection, KV append + GQA attention per (request, KV head), output
+    projection, gated MLP, residuals) at C2 (B=64, ctx 4096) on every host
+    core.  Bounded sample: one full layer is timed ``layer_samples`` times
+    (median) and the step is 32 x that (the 32 layers are identical).
+    Imports nothing from the product package.  Returns (step_s, info)."""
+    from oracle.decode_step import DecodeLayerF64, host_info, time_layers
+    c = C2_SHAPE
     t0 = time.perf_counter()
-    if ctx_mgr:
-        ctx_mgr.__enter__()
-    try:
-        with ThreadPoolExecutor(cores) as ex:
-            list(ex.map(worker, range(cores)))
-    finally:
-        if ctx_mgr:
-            ctx_mgr.__exit__(None, None, None)
-    dt = time.perf_counter() - t0
-    return sum(done) / dt, cores, sum(done)
-
-
-def job_items(model, world, batch, ctx):
-    """Work items (kv head, request) of one step over all ranks."""
-    import numpy as np
-    from paper_2511_14116_b200.placement import make_placement, owner_array
-    plan = make_placement("hybrid", model, range(world))
-    owner = owner_array(plan, model.num_kv_heads)
-    routing = route(batch, range(world), ctx)
-    n = 0
-    for row in owner:
-        tp = int((row >= 0).sum())
-        dp = int((row < 0).sum())
-        n += tp * batch + dp * batch  # every request once per head
-    return n
+    layer = DecodeLayerF64(c["hidden"], c["kv_heads"], c["qpk"], c["hd"], c["ffn"], c["batch"],
+                           c["ctx"])
+    setup_s = time.perf_counter() - t0
+    per_layer, times, cores = time_layers(layer, layer_samples)
+    del layer
+    info = host_info()
+    info.update({"setup_s": round(setup_s, 1), "layer_s": [round(t, 4) for t in times]})
+    return per_layer * c["layers"], info
 
 
 # ---------------------------------------------------------------- drivers --
 def run_reference(args, world, rank):
-    """--impl reference: the reference's CPU path for the hot path (the
-    oracle port of refexec._head_attention -- the reference itself is pure
-    Python/numpy and not present on the GPU box) on this host's cores."""
+    """--impl reference: the reference's CPU implementation of the path
+    (the float64 oracle port of refexec.py's decode step; the reference is
+    pure Python and cannot travel to the GPU box) on all host cores, rank 0
+    only; the other ranks exit without work.  Nothing from the product
+    package is imported (no product .so is loaded)."""
     if rank != 0:
         return
-    model = llama8b()
-    batch, ctx = 64, 4096
-    items = job_items(model, world, batch, ctx)
-    per_step = []
-    for i in range(args.warmup + args.steps):
-        rate, cores, done = cpu_oracle_rate(model.q_heads_per_kv_head, ctx,
-                                            seconds=args.ref_seconds)
-        if i >= args.warmup:
-            per_step.append(items / rate)
-    step_s = statistics.median(per_step)
-    value = batch / step_s
+    c = C2_SHAPE
+    step_s, info = cpu_decode_step(args.warmup + args.steps)
+    value = c["batch"] / step_s
+    sample = (f"each step = 32 x one float64 C2 decode layer (QKV, KV append + attention, "
+              f"O, gated MLP; B=64, ctx 4096), layer timed {args.warmup + args.steps} times "
+              f"(median) on {info['cores']} cores")
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(step_s * 1e3, 1), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(model, world, batch, ctx),
-            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores,
-                             "kind": "port",
-                             "sample": f"each step: {args.ref_seconds:.0f}s of float64 numpy "
-                                       f"decode items (qpk 4, ctx {ctx}) on {cores} threads, "
-                                       f"extrapolated to the {items} items of one step"},
+            "config": workload_config(world),
+            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": info["cores"],
+                             "kind": "port", "sample": sample, "host": info},
             "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def workload_config(model, world, batch, ctx):
+def workload_config(world, batch=64, ctx=4096):
+    c = C2_SHAPE
     return {"workload": "C2 Llama-3-8B-shaped hybrid-attention decode step, all 32 layers: "
                         "QKV GEMM, fused KV-append + paged GQA decode, O GEMM, TP MLP "
                         "partial (gate/up GEMM, swiglu, down GEMM); when N>1 the attention and MLP "
                         "partials are exchanged by fs_ar_residual (ordered sum + residual in one "
                         "kernel over IPC-mapped peer buffers; --exchange nccl: NCCL all-reduce)",
-            "layers": model.num_layers, "q_heads": model.num_q_heads,
-            "kv_heads": model.num_kv_heads, "head_dim": model.head_dim,
-            "hidden": model.hidden_dim, "batch": batch, "ctx": ctx, "world": world,
+            "layers": c["layers"], "q_heads": c["kv_heads"] * c["qpk"],
+            "kv_heads": c["kv_heads"], "head_dim": c["hd"], "hidden": c["hidden"],
+            "ffn": c["ffn"], "batch": batch, "ctx": ctx, "world": world,
             "placement": "hybrid", "page_tokens": 16, "parallelism": f"hybrid-tp{world}",
             "l2": "no flush: KV working set >> 126 MB L2 (34 GB at N=1)"}
 
@@ -591,8 +560,9 @@ def run_ours(args, world, rank, local_rank):
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "frac_of_nominal_8tbs": round(achieved / 8000.0, 4),
-                "kernel": "decode_kernel (fs_decode_attention: fused KV append + paged GQA "
-                          "decode + in-kernel split merge), one launch per layer",
+                "kernel": KERNEL_NAMES.get(args.kernel_config, f"config {args.kernel_config}") +
+                          " (fs_decode_attention: fused KV append + paged GQA decode + "
+                          "in-kernel split merge), one launch per layer",
                 "bytes_per_launch": int(per_launch_bytes),
                 "launch_ms": round(per_launch_ms, 5), "peak_source": peak_src,
                 "step_kv_frac": round(kv_step / (ms / 1e3) / 1e9 / peak, 4),
@@ -604,7 +574,7 @@ def run_ours(args, world, rank, local_rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (seeded random weights and KV)",
-            "config": workload_config(model, world, batch, ctx),
+            "config": workload_config(world, batch, ctx),
             "e2e": {"value": round(batch / (e2e_ms / 1e3), 1), "unit": UNIT,
                     "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                     "ms_per_step": round(e2e_ms, 4),
@@ -630,15 +600,13 @@ def run_ours(args, world, rank, local_rank):
             except ImportError:
                 pass
         if not args.skip_cpu:
-            rate, cores, done = cpu_oracle_rate(model.q_heads_per_kv_head, ctx,
-                                                seconds=args.cpu_seconds)
-            items = job_items(model, world, batch, ctx)
+            step_s, info = cpu_decode_step(args.cpu_layers)
             line["cpu_baseline"] = {
-                "value": round(batch / (items / rate), 4), "unit": UNIT, "cores": cores,
-                "kind": "port",
-                "sample": f"{done} float64 numpy decode items (qpk 4, ctx {ctx}) in "
-                          f"{args.cpu_seconds:.0f}s on {cores} threads, extrapolated to the "
-                          f"{items} items of one step"}
+                "value": round(batch / step_s, 4), "unit": UNIT, "cores": info["cores"],
+                "kind": "port", "host": info,
+                "sample": f"32 x one float64 C2 decode layer (oracle/decode_step.py: QKV, KV "
+                          f"append + attention, O, gated MLP; B=64, ctx 4096), median of "
+                          f"{args.cpu_layers} on {info['cores']} cores"}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -661,8 +629,8 @@ def main():
                          "buffers (default) or an NCCL all-reduce + add")
     ap.add_argument("--no-mlp", action="store_true",
                     help="attention sublayer only (no TP MLP partial / MLP all-reduce)")
-    ap.add_argument("--cpu-seconds", type=float, default=8.0)
-    ap.add_argument("--ref-seconds", type=float, default=4.0)
+    ap.add_argument("--cpu-layers", type=int, default=3,
+                    help="cpu_baseline sample: float64 C2 layers timed (median)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -44,6 +44,12 @@
  *                          transfers executed             recovery.py:430-504
  *   fs_copy_peer        <- recovery.plan_weight_recovery transfers executed
  *                          peer-to-peer over NVLink       recovery.py:396-427
+ *   fs_kv_backup_tokens <- advance_backup's drain of the tokens a decode step
+ *                          appends (token-granular)       recovery.py:193-247
+ *   fs_host_register    <- (new) the shared host mirrors the plans read from
+ *   fs_copy_2d / fs_copy_segments <- apply_weight_plan's pcie_host /
+ *                          nvlink_peer slices into the survivors' weights
+ *                                                          recovery.py:396-427, 591-600
  */
 #ifndef FAILSAFE_B200_H
 #define FAILSAFE_B200_H
@@ -152,7 +158,16 @@ typedef struct fs_decode_desc {
     int64_t partial_slots;     /* >= fs_decode_partial_slots(n_items)       */
     int32_t device;            /* CUDA device ordinal the launch runs on    */
     int32_t config;            /* 0 = default kernel configuration          */
+    int32_t flags;             /* FS_DECODE_* bits                          */
 } fs_decode_desc;
+
+/* fs_decode_desc.flags: the caller guarantees that the kernel launched
+ * immediately before on the stream writes none of page_off, item_len,
+ * item_seq, block_table or the pages (e.g. it is the projection GEMM), so
+ * the launch may read them and stage its first pages before its
+ * programmatic-dependent-launch wait.  Without the bit every read waits
+ * for the preceding kernel to complete (K3 / K4 / restores may precede). */
+#define FS_DECODE_EARLY_PREFETCH 1
 
 /* partial-result slots the stream-K split needs for n_items items
  * (config -1: enough for every kernel configuration) */
@@ -262,6 +277,45 @@ int fs_pages_scatter(void *kv_pool, const int32_t *page_ids, int32_t n_pages,
                      const void *src, const int32_t *src_slots, int32_t max_ctas,
                      void *stream);
 
+/* K5, token-granular (decode steps): for every item the token at
+ * item_len[i]-1 (512 B: its K and V rows) is copied from its page to the
+ * same page slot of `mirror` (FS_PAGE_BYTES per slot, slot == page id;
+ * typically mapped pinned host memory shared with the other ranks).
+ * Replaces advance_backup's per-step drain (recovery.py:193-247) of the
+ * tokens a decode step appends. */
+int fs_kv_backup_tokens(const void *kv_pool, const int32_t *block_table, int64_t bt_stride,
+                        const int32_t *item_seq, const int32_t *item_len, int32_t n_items,
+                        void *mirror, void *stream);
+
+/* Page-lock a host range (e.g. a /dev/shm mapping shared by the ranks of a
+ * node: the KV backup mirror and the weight store outlive the process that
+ * wrote them) for zero-copy / DMA access; *dev_ptr = its device address. */
+int fs_host_register(void *ptr, int64_t bytes, void **dev_ptr);
+int fs_host_unregister(void *ptr);
+
+/* K7 transfer primitive: 2-D copy (rows of `width` bytes) between any of
+ * registered host memory, local device memory and a peer's device memory
+ * mapped by CUDA IPC (NVLink); apply_weight_plan's pcie_host and
+ * nvlink_peer slices (recovery.py:396-427, 591-600). */
+int fs_copy_2d(void *dst, int64_t dpitch, const void *src, int64_t spitch, int64_t width,
+               int64_t height, void *stream);
+
+/* K7 executor: ONE launch performing n_segs 2-D copies (segs and row_off
+ * in device memory; row_off[i] = sum of heights before segment i, n_segs+1
+ * entries).  src / dst may be local HBM, peer HBM mapped by CUDA IPC
+ * (NVLink) or mapped pinned host memory (fs_host_register; PCIe).  Used to
+ * execute apply_weight_plan (recovery.py:591-600): the plan's pcie_host
+ * slices, its nvlink_peer remainders and the scatter of the recovered
+ * shards into a survivor's fused weight tensors.  ctas <= 0: 4 per SM. */
+typedef struct fs_copy_seg {
+    const void *src;
+    void *dst;
+    int64_t spitch, dpitch;   /* bytes between rows                        */
+    int64_t width, height;    /* bytes per row, rows                       */
+} fs_copy_seg;
+int fs_copy_segments(const fs_copy_seg *segs, const int64_t *row_off, int32_t n_segs,
+                     int32_t ctas, void *stream);
+
 /* Skinny weight-streaming GEMM of the decode step (tcgen05.mma + TMA,
  * stream-K over (128-column tile, 64-k) units, persistent grid):
  *   STORE    (0): out[n, c]  = sum_k x[n, k] W[k, c]
@@ -320,6 +374,10 @@ int fs_ar_residual(void *const *peers, int32_t rank, int32_t world, int64_t n,
 int fs_enable_peer(int device, int peer);
 int fs_copy_peer(void *dst, int dst_device, const void *src, int src_device,
                  int64_t bytes, void *stream);
+
+/* Debugging (tools/gemm_tl.py): per-CTA globaltimer phase stamps of the
+ * skinny GEMM are written to dev_buf while it is non-NULL. */
+void fs_gemm_debug_timestamps(unsigned long long *dev_buf);
 
 #ifdef __cplusplus
 }

@@ -39,8 +39,11 @@ class DecodeDesc(C.Structure):
         ("item_sem", C.c_void_p), ("n_items", C.c_int32), ("q_per_kv", C.c_int32), ("scale", C.c_float),
         ("out_fp32", C.c_int32), ("out", C.c_void_p), ("part_o", C.c_void_p),
         ("part_lse", C.c_void_p), ("partial_slots", C.c_int64), ("device", C.c_int32),
-        ("config", C.c_int32),
+        ("config", C.c_int32), ("flags", C.c_int32),
     ]
+
+
+DECODE_EARLY_PREFETCH = 1  # FS_DECODE_EARLY_PREFETCH
 
 
 class PrefillDesc(C.Structure):
@@ -93,6 +96,13 @@ _SIGS = {
                                   C.c_int32, C.c_void_p]),
     "fs_pages_scatter": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                                    C.c_int32, C.c_void_p]),
+    "fs_kv_backup_tokens": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                      C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    "fs_host_register": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_void_p)]),
+    "fs_host_unregister": (C.c_int, [C.c_void_p]),
+    "fs_copy_2d": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int64,
+                             C.c_int64, C.c_void_p]),
+    "fs_copy_segments": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     "fs_gemm_workspace_floats": (C.c_int64, [C.c_int, C.c_int32, C.c_int32]),
     "fs_gemm_skinny": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p,
                                  C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p,
@@ -114,6 +124,7 @@ _SIGS = {
     "fs_enable_peer": (C.c_int, [C.c_int, C.c_int]),
     "fs_copy_peer": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int64,
                                C.c_void_p]),
+    "fs_gemm_debug_timestamps": (None, [C.c_void_p]),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -35,15 +35,18 @@ class FusedExchange:
     """Two symmetric exchange buffers of this rank and their peer mappings.
 
     ``group``: the torch.distributed group of the alive ranks (any backend;
-    used once to swap IPC handles); ``max_elems``: largest partial (bf16
-    elements, e.g. batch x hidden).  All ranks must construct it together.
+    used once to swap IPC handles) or a :class:`cluster.StoreControl` (the
+    store-based control plane that survives a dead rank); ``max_elems``:
+    largest partial (bf16 elements, e.g. batch x hidden).  All ranks must
+    construct it together.
     """
 
     def __init__(self, group, max_elems: int, device=None, check: bool = True):
         self.device = torch.device(device if device is not None else "cuda")
         dev = self.device.index if self.device.index is not None else torch.cuda.current_device()
-        self.rank = dist.get_rank(group)
-        self.world = dist.get_world_size(group)
+        ctl = group if hasattr(group, "all_gather_object") else None
+        self.rank = ctl.index if ctl else dist.get_rank(group)
+        self.world = ctl.world if ctl else dist.get_world_size(group)
         if self.world > N.FS_AR_MAX_WORLD:
             raise ValidationError(f"fused exchange supports up to {N.FS_AR_MAX_WORLD} ranks")
         self.max_elems = int(max_elems) + (-int(max_elems)) % 8
@@ -58,8 +61,11 @@ class FusedExchange:
             h = (C.c_uint8 * 64)()
             N.check(N.lib.fs_ar_ipc_handle(C.c_void_p(p.value), h), "fs_ar_ipc_handle")
             handles.append(bytes(h))
-        every = [None] * self.world
-        dist.all_gather_object(every, handles, group=group)
+        if ctl:
+            every = ctl.all_gather_object(handles)
+        else:
+            every = [None] * self.world
+            dist.all_gather_object(every, handles, group=group)
         self.peers = []
         for i in range(2):
             arr = (C.c_void_p * self.world)()
@@ -75,7 +81,10 @@ class FusedExchange:
             self.peers.append(arr)
         self._views = [torch.as_tensor(_DeviceArray(p, self.max_elems), device=self.device)
                        .view(torch.bfloat16) for p in self._own]
-        dist.barrier(group=group)
+        if ctl:
+            ctl.barrier()
+        else:
+            dist.barrier(group=group)
         if check:
             self._self_check()
 

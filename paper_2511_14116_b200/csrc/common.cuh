@@ -173,6 +173,15 @@ __device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
     return r;
 }
 
+// as pack_f16, saturating to +-65504 (split partials O / l: a convex
+// combination of f16 V rows, marginally above 65504 at most from the f16 P
+// vs fp32 l rounding -- never Inf)
+__device__ __forceinline__ uint32_t pack_f16_sat(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
 // (lo, hi) as a bf16x2 pair plus the bf16x2 pair of its rounding residual:
 // h + l carries ~16 mantissa bits (two bf16 MMAs instead of one)
 __device__ __forceinline__ void split_bf16x2(float lo, float hi, uint32_t &h, uint32_t &l) {

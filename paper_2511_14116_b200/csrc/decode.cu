@@ -50,6 +50,7 @@ struct DecodeParams {
     float *part_o, *part_lse;
     int64_t n_warps;  // W of the stream-K partition
     int32_t tab_cache;  // decode_cta_kernel: page_off / item_seq staged in smem (n_items <= kTabItems)
+    int32_t early;      // FS_DECODE_EARLY_PREFETCH: tables + first pages read before griddepcontrol.wait
 };
 
 // items whose page offsets and block-table rows decode_cta_kernel stages in
@@ -187,6 +188,9 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) decode_kernel(const DecodePa
     extern __shared__ __align__(1024) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
+    // without the caller's guarantee that the preceding kernel writes none
+    // of the tables / pages, every read stays behind the PDL wait
+    if (!p.early) grid_dependency_wait();
 
     const int64_t P = p.page_off[p.n_items];
     const int64_t W = p.n_warps;
@@ -516,9 +520,10 @@ static int launch_decode(const DecodeParams &prm, int sms, cudaStream_t st) {
         FS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set[dev & 63] = true;
     }
-    // PDL: the prologue (table lookups, first TMA page loads) may overlap the
-    // tail of the preceding kernel; the kernel waits (griddepcontrol.wait)
-    // before its first read of q / kv_new and before any global write.
+    // PDL: with FS_DECODE_EARLY_PREFETCH the prologue (table lookups, first
+    // TMA page loads) may overlap the tail of the preceding kernel and the
+    // kernel waits (griddepcontrol.wait) before its first read of q / kv_new
+    // and before any global write; without it the wait comes first.
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(sms * CTAS);
     lc.blockDim = dim3(WARPS * 32);
@@ -605,6 +610,7 @@ extern "C" int fs_decode_attention(const fs_decode_desc *d, void *stream) {
     prm.part_o = d->part_o;
     prm.part_lse = d->part_lse;
     prm.n_warps = W;
+    prm.early = (d->flags & FS_DECODE_EARLY_PREFETCH) ? 1 : 0;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (d->config) {
 #define FS_CFG_CASE(i, w, s, c, k) \

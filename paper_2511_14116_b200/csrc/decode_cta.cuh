@@ -26,6 +26,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_cta_kernel(const DecodeP
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
     constexpr int NT = WARPS * 32;
+    if (!p.early) grid_dependency_wait();  // see decode_kernel
 
     // page offsets + block-table rows of all items -> smem in one round
     // trip (the first page copy then waits for one dependent load, the

@@ -106,9 +106,126 @@ __global__ void __launch_bounds__(256) page_copy_kernel(uint8_t *pool, const int
     }
 }
 
+// K5, token-granular: the token at item_len[i]-1 of every item -> the same
+// page slot of the host mirror (slot == page id).  A token is 4 x 128 B of
+// the page (K / V half x the two 64-dim atoms; the swizzle permutes chunks
+// only within a 128-B row piece): one warp per item, lane = 16-B chunk.
+__global__ void __launch_bounds__(256) kv_backup_tokens_kernel(const uint8_t *pool,
+                                                               const int32_t *bt, int64_t bt_stride,
+                                                               const int32_t *item_seq,
+                                                               const int32_t *item_len,
+                                                               int32_t n_items, uint8_t *mirror) {
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= n_items) return;
+    const int32_t len = item_len[i];
+    if (len <= 0) return;
+    const int32_t pos = len - 1;
+    const int64_t page = bt[(int64_t)item_seq[i] * bt_stride + pos / kPageTokens];
+    const int piece = lane >> 3;
+    const int64_t off = page * kPageBytes + (piece >> 1) * kHalfPage + (piece & 1) * 2048 +
+                        (pos % kPageTokens) * 128 + (lane & 7) * 16;
+    *reinterpret_cast<uint4 *>(mirror + off) = *reinterpret_cast<const uint4 *>(pool + off);
+}
+
+// K7 executor: many 2-D copies in ONE launch.  Each segment is `height`
+// rows of `width` bytes; a warp copies one row (16-B lanes when source,
+// destination, pitches and width are 16-B aligned, bytes otherwise), rows
+// are dealt to warps round-robin over the flattened row space (row_off =
+// exclusive prefix of heights).  Sources / destinations may be local HBM,
+// a peer's HBM mapped by CUDA IPC (the reads then run over NVLink) or
+// mapped pinned host memory (PCIe): the SMs keep ~thousands of 16-B loads
+// in flight, which is what a P2P or zero-copy stream needs.
+__global__ void __launch_bounds__(256) copy_segments_kernel(const fs_copy_seg *segs,
+                                                            const int64_t *row_off, int32_t n_segs) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t total = row_off[n_segs];
+    for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < total; g += warps) {
+        int lo = 0, hi = n_segs;  // row_off[lo] <= g < row_off[hi]
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (row_off[mid] <= g) lo = mid;
+            else hi = mid;
+        }
+        const fs_copy_seg sg = segs[lo];
+        const int64_t row = g - row_off[lo];
+        const uint8_t *src = static_cast<const uint8_t *>(sg.src) + row * sg.spitch;
+        uint8_t *dst = static_cast<uint8_t *>(sg.dst) + row * sg.dpitch;
+        const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) |
+                           (uintptr_t)sg.width) & 15) == 0;
+        if (vec) {
+            const int64_t n16 = sg.width >> 4;
+            const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+            uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+            int64_t i = lane;
+            for (; i + 96 < n16; i += 128) {  // 4 loads in flight per lane
+                const uint4 a = s4[i], b = s4[i + 32], c = s4[i + 64], d = s4[i + 96];
+                d4[i] = a;
+                d4[i + 32] = b;
+                d4[i + 64] = c;
+                d4[i + 96] = d;
+            }
+            for (; i < n16; i += 32) d4[i] = s4[i];
+        } else {
+            for (int64_t i = lane; i < sg.width; i += 32) dst[i] = src[i];
+        }
+    }
+}
+
 }  // namespace fs
 
 using namespace fs;
+
+extern "C" int fs_copy_segments(const fs_copy_seg *segs, const int64_t *row_off, int32_t n_segs,
+                                int32_t ctas, void *stream) {
+    FS_CHECK_ARG(n_segs >= 0, "n_segs must be nonnegative");
+    if (n_segs == 0) return FS_OK;
+    FS_CHECK_ARG(segs && row_off, "null pointer");
+    copy_segments_kernel<<<ctas > 0 ? ctas : 4 * 148, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        segs, row_off, n_segs);
+    return cuda_status(cudaGetLastError(), "copy_segments_kernel launch");
+}
+
+extern "C" int fs_kv_backup_tokens(const void *kv_pool, const int32_t *block_table,
+                                   int64_t bt_stride, const int32_t *item_seq,
+                                   const int32_t *item_len, int32_t n_items, void *mirror,
+                                   void *stream) {
+    FS_CHECK_ARG(n_items >= 0, "n_items must be nonnegative");
+    if (n_items == 0) return FS_OK;
+    FS_CHECK_ARG(kv_pool && block_table && item_seq && item_len && mirror, "null pointer");
+    FS_CHECK_ARG((reinterpret_cast<uintptr_t>(mirror) & 15) == 0, "mirror must be 16B aligned");
+    const int64_t threads = (int64_t)n_items * 32;
+    kv_backup_tokens_kernel<<<(unsigned)((threads + 255) / 256), 256, 0,
+                              static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint8_t *>(kv_pool), block_table, bt_stride, item_seq, item_len,
+        n_items, static_cast<uint8_t *>(mirror));
+    return cuda_status(cudaGetLastError(), "kv_backup_tokens_kernel launch");
+}
+
+extern "C" int fs_host_register(void *ptr, int64_t bytes, void **dev_ptr) {
+    FS_CHECK_ARG(ptr && bytes > 0 && dev_ptr, "null pointer or empty range");
+    FS_CUDA(cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterPortable | cudaHostRegisterMapped));
+    FS_CUDA(cudaHostGetDevicePointer(dev_ptr, ptr, 0));
+    return FS_OK;
+}
+
+extern "C" int fs_host_unregister(void *ptr) {
+    FS_CHECK_ARG(ptr, "null pointer");
+    FS_CUDA(cudaHostUnregister(ptr));
+    return FS_OK;
+}
+
+extern "C" int fs_copy_2d(void *dst, int64_t dpitch, const void *src, int64_t spitch,
+                          int64_t width, int64_t height, void *stream) {
+    FS_CHECK_ARG(width >= 0 && height >= 0, "negative extent");
+    if (width == 0 || height == 0) return FS_OK;
+    FS_CHECK_ARG(dst && src, "null pointer");
+    FS_CHECK_ARG(dpitch >= width && spitch >= width, "pitch smaller than width");
+    FS_CUDA(cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width,
+                              (size_t)height, cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+    return FS_OK;
+}
 
 extern "C" int fs_kv_write(void *kv_pool, const int32_t *block_table, int64_t bt_stride,
                            const int32_t *tok_seq, const int32_t *tok_pos, const int32_t *tok_src,

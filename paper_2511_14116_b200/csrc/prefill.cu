@@ -274,8 +274,8 @@ __global__ void __launch_bounds__((kConsumerWarps + 2) * 32) prefill_kernel(cons
 #pragma unroll
         for (int nt = 0; nt < 16; ++nt) {
             const int d = nt * 8 + 2 * tig;
-            *reinterpret_cast<uint32_t *>(po + ra * kHeadDim + d) = pack_f16(o[nt][0] * ia, o[nt][1] * ia);
-            *reinterpret_cast<uint32_t *>(po + rb * kHeadDim + d) = pack_f16(o[nt][2] * ib, o[nt][3] * ib);
+            *reinterpret_cast<uint32_t *>(po + ra * kHeadDim + d) = pack_f16_sat(o[nt][0] * ia, o[nt][1] * ia);
+            *reinterpret_cast<uint32_t *>(po + rb * kHeadDim + d) = pack_f16_sat(o[nt][2] * ib, o[nt][3] * ib);
         }
         if (tig == 0) {
             p.part_lse[(int64_t)slot * kTileRows + ra] = la > 0.f ? ma + __log2f(la) : -INFINITY;

@@ -303,6 +303,11 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
                     bulk_g2s_plain(vs + a * kAtom + pp * 2048, src + kHalfPage, kAtomBytes, v_full + 8 * st);
             }
         }
+        // consume the ring-slot releases of the last blocks (the MMA warp
+        // commits them; they retire before o_done, so these waits return at
+        // once): no barrier phase is left unconsumed at exit (synccheck)
+        for (int j = max(nb - kKS, 0); j < nb; ++j) mbar_wait(k_empty + 8 * (j % kKS), (j / kKS) & 1);
+        for (int j = max(nb - kVS, 0); j < nb; ++j) mbar_wait(v_empty + 8 * (j % kVS), (j / kVS) & 1);
     } else if (warp == kSoftWarps + 1) {
         // ---------------- MMA issuer ----------------
         // The whole warp runs the loop so descriptors and TMEM addresses are
@@ -513,6 +518,9 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
         // ---- epilogue: O / l (or the split partial) ----
         grid_launch_dependents();  // the combine launch (PDL) may be scheduled now
         mbar_wait(o_done + 8 * (2 * h + ((nb - 1) % kSBuf)), ((nb - 1) / kSBuf) & 1);
+        // (two S buffers: also consume the other buffer's last commit, which
+        // retired earlier, so no barrier phase is left unconsumed at exit)
+        if (kSBuf == 2 && nb >= 2) mbar_wait(o_done + 8 * (2 * h + ((nb - 2) % kSBuf)), ((nb - 2) / kSBuf) & 1);
         tc_after();
         const float inv = l > 0.f ? 1.f / l : 0.f;
         const int slot = p.tile_slot[t];
@@ -542,8 +550,8 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
             const int Rr = wrow0 + rr;
             if (slot >= 0) {  // f16 partial: 4 dims = 8 B per lane
                 uint2 hv;
-                hv.x = pack_f16(v.x, v.y);
-                hv.y = pack_f16(v.z, v.w);
+                hv.x = pack_f16_sat(v.x, v.y);
+                hv.y = pack_f16_sat(v.z, v.w);
                 reinterpret_cast<uint2 *>(p.part_o + ((int64_t)slot * rows + Rr) * kHeadDim)[lane] = hv;
                 continue;
             }

@@ -116,7 +116,8 @@ class HybridDecodeRank:
     def __init__(self, model: ModelSpec, owner, rank: int, routing, batch: int, capacity: int,
                  device=None, seed: int = 0, group=None, page_order: str = "contiguous",
                  config: int = 0, mlp: bool = False, shard_owner=None, gemm: str = "cublas",
-                 request_capacity=None, exchange: str = "nccl", exchange_elems: int = None):
+                 request_capacity=None, exchange: str = "nccl", exchange_elems: int = None,
+                 reserve_pages: int = 0):
         if model.head_dim != N.HEAD_DIM:
             raise ValidationError(f"head_dim must be {N.HEAD_DIM} for the CUDA path")
         self.model = model
@@ -129,12 +130,16 @@ class HybridDecodeRank:
         self.work = RankWork.build(np.asarray(owner, dtype=np.int32), rank, routing, batch)
         self.cache = PagedKVCache(self.work, capacity, self.qpk, self.device,
                                   page_order=page_order, seed=seed, config=config,
-                                  request_capacity=request_capacity)
+                                  request_capacity=request_capacity, reserve_pages=reserve_pages)
+        self.backup_ptr = None  # token-granular K5 target (hostmirror.KVMirror), if any
         hd, hid, S = model.head_dim, model.hidden_dim, self.work.n_slots
         self.n_slots = S
         L = model.num_layers
         dev = self.device
         rw = self.cache.set_fused_layout()   # [q slots | k slots | v slots]
+        # every decode launch of the step directly follows the QKV GEMM,
+        # which writes only qkv: K1 may stage its first pages under PDL
+        self.cache.early_prefetch = True
         qw = S * self.qpk * hd
         s_in, s_o, _ = _scales(model)
         self.wqkv = torch.zeros((L, hid, rw), dtype=torch.bfloat16, device=dev)
@@ -153,9 +158,12 @@ class HybridDecodeRank:
         self.part = torch.empty((batch, hid), dtype=torch.bfloat16, device=dev)
         self.x = torch.zeros((batch, hid), dtype=torch.bfloat16, device=dev)
         self.ffn_cols = np.zeros(0, dtype=np.int32)
+        self.shards = []
+        self.num_shards = len(shard_owner) if shard_owner is not None else 0
         if mlp:
             if shard_owner is None:
                 raise ValidationError("mlp=True needs the FFN shard owner table")
+            self.shards = sorted(s_ for s_, g in enumerate(shard_owner) if g == rank)
             self.ffn_cols = ffn_columns(model, shard_owner, rank)
             C = len(self.ffn_cols)
             self.w_gu = torch.empty((L, hid, 2 * C), dtype=torch.bfloat16, device=dev)
@@ -276,6 +284,11 @@ class HybridDecodeRank:
                 x.add_(self.part)
 
     def _layers(self) -> None:
+        self._layers_inner()
+        if self.backup_ptr is not None:
+            self.backup_tokens()
+
+    def _layers_inner(self) -> None:
         if self.gemm == "tcgen05":
             return self._layers_skinny()
         B, S, hd = self.batch, self.n_slots, self.model.head_dim
@@ -314,6 +327,154 @@ class HybridDecodeRank:
                     torch.distributed.all_reduce(self.part, group=self.group)
                     x.add_(self.part)
 
+    # ------------------------------------------------ failover (in place) --
+    def _head_parts(self, layer: int, j: int, wqkv=None, wo=None, S=None):
+        """Slot ``j`` of ``layer`` in the fused weights as the 4 parts of a
+        canonical head piece (hostmirror.WeightLayout), in piece order:
+        [(address, row pitch, row bytes, rows, offset in the piece)]."""
+        wqkv = self.wqkv if wqkv is None else wqkv
+        wo = self.wo if wo is None else wo
+        S = self.n_slots if S is None else S
+        hd, qpk, hid = self.model.head_dim, self.qpk, self.model.hidden_dim
+        qw, rw = S * qpk * hd, wqkv.shape[2]
+        base = wqkv.data_ptr() + layer * hid * rw * 2
+        qb, kb = hid * qpk * hd * 2, hid * hd * 2
+        o_addr = wo.data_ptr() + (layer * wo.shape[1] + j * qpk * hd) * hid * 2
+        return [(base + j * qpk * hd * 2, rw * 2, qpk * hd * 2, hid, 0),          # Wq
+                (base + (qw + j * hd) * 2, rw * 2, hd * 2, hid, qb),              # Wk
+                (base + (qw + (S + j) * hd) * 2, rw * 2, hd * 2, hid, qb + kb),   # Wv
+                (o_addr, qpk * hd * hid * 2, qpk * hd * hid * 2, 1, qb + 2 * kb)]  # Wo
+
+    def _shard_parts(self, layer: int, k: int, w_gu=None, w_d=None):
+        """Local FFN shard ``k`` of ``layer`` as the parts of a canonical
+        shard piece ``[Wg | Wu | Wd]`` (same tuple format)."""
+        w_gu = self.w_gu if w_gu is None else w_gu
+        w_d = self.w_d if w_d is None else w_d
+        hid = self.model.hidden_dim
+        w = self.model.ffn_intermediate_dim // self.num_shards
+        C2 = w_gu.shape[2]
+        base = w_gu.data_ptr() + layer * hid * C2 * 2
+        d_addr = w_d.data_ptr() + (layer * w_d.shape[1] + k * w) * hid * 2
+        return [(base + k * w * 2, C2 * 2, w * 2, hid, 0),                        # Wg
+                (base + (C2 // 2 + k * w) * 2, C2 * 2, w * 2, hid, hid * w * 2),   # Wu
+                (d_addr, w * hid * 2, w * hid * 2, 1, 2 * hid * w * 2)]            # Wd
+
+    @staticmethod
+    def _to_piece(seg, parts, piece: int) -> None:
+        for addr, pitch, width, rows, off in parts:
+            seg.add(piece + off, width, addr, pitch, width, rows)
+
+    @staticmethod
+    def _from_piece(seg, parts, piece: int) -> None:
+        for addr, pitch, width, rows, off in parts:
+            seg.add(addr, pitch, piece + off, width, width, rows)
+
+    @staticmethod
+    def _between(seg, src_parts, dst_parts) -> None:
+        for (sa, sp, width, rows, _), (da, dp, _, _, _) in zip(src_parts, dst_parts):
+            seg.add(da, dp, sa, sp, width, rows)
+
+    def publish_weights(self, store, heads=None) -> int:
+        """Write this rank's weight pieces into the node's host weight
+        store (hostmirror.WeightStore): its TP heads (or ``heads``: per
+        layer the head ids to publish) and its FFN shards.  One launch
+        (D2H over PCIe into the mapped store); returns bytes written."""
+        from .hostmirror import SegmentCopy
+        if self.gemm != "cublas":
+            raise ValidationError("publish_weights needs the cuBLAS weight layout")
+        lay = store.layout
+        seg = SegmentCopy()
+        for layer in range(self.model.num_layers):
+            sel = heads[layer] if heads is not None else \
+                self.work.slot_heads[layer][:self.work.n_tp[layer]]
+            for j, h in enumerate(self.work.slot_heads[layer]):
+                if h in sel:
+                    self._to_piece(seg, self._head_parts(layer, j),
+                                   store.dev_ptr + lay.head_off(layer, h))
+            if self.mlp:
+                for k, sh in enumerate(self.shards):
+                    self._to_piece(seg, self._shard_parts(layer, k),
+                                   store.dev_ptr + lay.shard_off(layer, sh))
+        seg.run(self.device)
+        return seg.bytes
+
+    def adopt(self, owner, routing, shard_owner, pieces) -> np.ndarray:
+        """Adopt a new placement IN PLACE (the on-demand shrink target,
+        recovery.py:396-427, after re-routing): KV pages of every (layer,
+        head, request) the rank keeps stay where they are (new items get
+        reserve pages, PagedKVCache.adopt); the fused weights are re-laid
+        out for the new slots in ONE copy launch -- kept slots / shards from
+        the current tensors, new ones from ``pieces``: {("head", layer,
+        head) | ("shard", layer, shard): device address of the canonical
+        piece} (the K7 staging buffer).  Returns the new items (their KV is
+        restored by the caller).  The step graph must be captured again."""
+        from .hostmirror import SegmentCopy
+        if self.gemm != "cublas":
+            raise ValidationError("adopt needs the cuBLAS weight layout")
+        old_work = self.work
+        work = RankWork.build(np.asarray(owner, dtype=np.int32), self.rank, routing, self.batch)
+        L, hd, hid, qpk = self.model.num_layers, self.model.head_dim, self.model.hidden_dim, self.qpk
+        S = work.n_slots
+        rw = S * (qpk + 2) * hd
+        dev = self.device
+        wqkv = torch.zeros((L, hid, rw), dtype=torch.bfloat16, device=dev)
+        wo = torch.zeros((L, S * qpk * hd, hid), dtype=torch.bfloat16, device=dev)
+        seg = SegmentCopy()
+        for layer in range(L):
+            old_heads = old_work.slot_heads[layer]
+            for j, h in enumerate(work.slot_heads[layer]):
+                new_parts = self._head_parts(layer, j, wqkv=wqkv, wo=wo, S=S)
+                if h in old_heads:  # kept slot: straight from the current tensors
+                    self._between(seg, self._head_parts(layer, old_heads.index(h)), new_parts)
+                else:
+                    key = ("head", layer, h)
+                    if key not in pieces:
+                        raise SimulationError(f"no recovered weights for layer {layer} head {h}")
+                    self._from_piece(seg, new_parts, pieces[key])
+        shards = self.shards
+        if self.mlp:
+            shards = sorted(s_ for s_, g in enumerate(shard_owner) if g == self.rank)
+            C = len(shards) * (self.model.ffn_intermediate_dim // self.num_shards)
+            w_gu = torch.zeros((L, hid, 2 * C), dtype=torch.bfloat16, device=dev)
+            w_d = torch.zeros((L, C, hid), dtype=torch.bfloat16, device=dev)
+            for layer in range(L):
+                for k, sh in enumerate(shards):
+                    new_parts = self._shard_parts(layer, k, w_gu=w_gu, w_d=w_d)
+                    if sh in self.shards:
+                        self._between(seg, self._shard_parts(layer, self.shards.index(sh)),
+                                      new_parts)
+                    else:
+                        key = ("shard", layer, sh)
+                        if key not in pieces:
+                            raise SimulationError(f"no recovered weights for layer {layer} "
+                                                  f"shard {sh}")
+                        self._from_piece(seg, new_parts, pieces[key])
+        seg.run(dev)
+        torch.cuda.current_stream(dev).synchronize()
+        fresh = self.cache.adopt(work)
+        self.work, self.n_slots = work, S
+        self.wqkv, self.wo = wqkv, wo
+        if self.mlp:
+            self.w_gu, self.w_d, self.shards = w_gu, w_d, shards
+            self.ffn_cols = ffn_columns(self.model, shard_owner, self.rank)
+            C = len(self.ffn_cols)
+            self.h = torch.empty((self.batch, 2 * C), dtype=torch.bfloat16, device=dev)
+            self.act = torch.empty((self.batch, C), dtype=torch.bfloat16, device=dev)
+        self.qkv = torch.empty((self.batch, rw), dtype=torch.bfloat16, device=dev)
+        self.o = torch.zeros((self.batch * S, qpk, hd), dtype=torch.bfloat16, device=dev)
+        self._graph = None
+        return fresh
+
+    def backup_tokens(self) -> None:
+        """K5 (token-granular): the token each item appended this step ->
+        the rank's host mirror (``self.backup_ptr``), one launch."""
+        c = self.cache
+        N.check(N.lib.fs_kv_backup_tokens(N.ptr(c.pool), N.ptr(c.block_table), c.pages_per_seq,
+                                          N.ptr(c.item_seq), N.ptr(c.item_len), c.work.n_items,
+                                          N.C.c_void_p(self.backup_ptr), N.C.c_void_p(
+                                              torch.cuda.current_stream(self.device).cuda_stream)),
+                "fs_kv_backup_tokens")
+
     def launches_per_step(self) -> int:
         """Our kernel launches per step: the fused decode launch per layer,
         plus the swiglu launch per layer with the MLP (cuBLAS GEMMs), or the
@@ -325,6 +486,8 @@ class HybridDecodeRank:
         n = self.model.num_layers * (2 if has_mlp else 1)
         if self.xchg is not None:  # one fs_ar_residual per exchange
             n += self.model.num_layers * (2 if self.mlp else 1)
+        if self.backup_ptr is not None:  # token backup
+            n += 1
         return n
 
     def weight_bytes(self) -> int:
@@ -340,8 +503,12 @@ class HybridDecodeRank:
         """Capture one decode step (all layers) into a CUDA graph."""
         s = torch.cuda.Stream(device=self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
+        x_saved = self.x.clone()
         with torch.cuda.stream(s):
             self._layers()  # warm cuBLAS workspaces outside capture
+            # the warm-up must not advance the state: x back; the token it
+            # appended at len-1 is rewritten by the next step
+            self.x.copy_(x_saved)
         torch.cuda.current_stream(self.device).wait_stream(s)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):

@@ -77,10 +77,32 @@ class RankWork:
                    slot_heads=slot_heads, n_tp=n_tp, seg_items=np.array(seg, dtype=np.int32),
                    item_req=cat(reqs), item_slot=cat(slots), item_head=cat(heads))
 
+    def keys(self) -> np.ndarray:
+        return item_keys(self)
+
     def kv_tokens(self, lens) -> int:
         """KV tokens resident on this rank for per-request lengths ``lens``."""
         lens = np.asarray(lens, dtype=np.int64)
         return int(lens[self.item_req].sum()) if self.n_items else 0
+
+
+def item_keys(work: RankWork) -> np.ndarray:
+    """Per item the packed key (layer << 40) | (head << 20) | request."""
+    if not work.n_items:
+        return np.zeros(0, np.int64)
+    layer = np.repeat(np.arange(work.num_layers, dtype=np.int64), np.diff(work.seg_items))
+    return (layer << 40) | (work.item_head.astype(np.int64) << 20) | work.item_req.astype(np.int64)
+
+
+def unpack_keys(keys: np.ndarray) -> np.ndarray:
+    """[n, 3] int32 (layer, head, request) of packed item keys."""
+    keys = np.asarray(keys, dtype=np.int64)
+    return np.stack([keys >> 40, (keys >> 20) & 0xFFFFF, keys & 0xFFFFF], axis=1).astype(np.int32)
+
+
+def pack_keys(lhr: np.ndarray) -> np.ndarray:
+    lhr = np.asarray(lhr, dtype=np.int64).reshape(-1, 3)
+    return (lhr[:, 0] << 40) | (lhr[:, 1] << 20) | lhr[:, 2]
 
 
 def _stream():
@@ -102,45 +124,67 @@ class PagedKVCache:
 
     def __init__(self, work: RankWork, capacity: int, q_per_kv: int, device=None,
                  page_order: str = "contiguous", seed: int = 0, config: int = 0,
-                 request_capacity=None):
+                 request_capacity=None, reserve_pages: int = 0):
         if not (1 <= q_per_kv <= N.MAX_Q_PER_KV):
             raise ValidationError(f"q_per_kv must be in [1, {N.MAX_Q_PER_KV}]")
         if capacity < 1:
             raise ValidationError("capacity must be >= 1 token")
-        self.work = work
+        if reserve_pages < 0:
+            raise ValidationError("reserve_pages must be nonnegative")
         self.qpk = q_per_kv
         self.capacity = capacity
         self.config = config
         self.device = torch.device(device if device is not None else "cuda")
         self.dev_index = self.device.index if self.device.index is not None \
             else torch.cuda.current_device()
-        n_seq = work.n_items
         self.pages_per_seq = math.ceil(capacity / N.PAGE_TOKENS)
-        if request_capacity is None:
-            seq_pages = np.full(n_seq, self.pages_per_seq, dtype=np.int64)
-        else:
-            # per-request token capacity (<= capacity): only those pages are
-            # backed; the rest of each block-table row is never addressed
-            cap = np.asarray(request_capacity, dtype=np.int64)
-            if cap.size and (cap.max() > capacity or cap.min() < 0):
-                raise ValidationError("request capacities must lie in [0, capacity]")
-            seq_pages = (cap[work.item_req] + N.PAGE_TOKENS - 1) // N.PAGE_TOKENS \
-                if n_seq else np.zeros(0, np.int64)
-        self.seq_tokens = seq_pages * N.PAGE_TOKENS
-        self.n_pages = max(1, int(seq_pages.sum()))
+        self.request_capacity = None if request_capacity is None else \
+            np.asarray(request_capacity, dtype=np.int64)
+        cap = self.request_capacity
+        if cap is not None and cap.size and (cap.max() > capacity or cap.min() < 0):
+            raise ValidationError("request capacities must lie in [0, capacity]")
+        seq_pages = self._seq_pages(work.item_req)
+        used = int(seq_pages.sum())
+        # reserve: free pages for the items an on-demand adoption adds
+        # (replicated heads of a failed GPU, re-routed requests)
+        self.n_pages = max(1, used + reserve_pages)
         ids = np.arange(self.n_pages, dtype=np.int64)
         if page_order == "shuffled":
             ids = np.random.default_rng(seed).permutation(self.n_pages)
         elif page_order != "contiguous":
             raise ValidationError(f"unknown page_order {page_order!r}")
-        bt = np.zeros((max(n_seq, 0), self.pages_per_seq), dtype=np.int64)
+        self.page_order = page_order
+        bt = np.zeros((work.n_items, self.pages_per_seq), dtype=np.int64)
         cols = np.arange(self.pages_per_seq)
         mask = cols[None, :] < seq_pages[:, None]
-        bt[mask] = ids[:int(seq_pages.sum())]
-        dev = self.device
+        bt[mask] = ids[:used]
+        self.free_pages = list(ids[used:])
         # zero-filled: unwritten rows hold finite values (0), never NaN bit patterns
-        self.pool = torch.zeros((self.n_pages, N.PAGE_BYTES), dtype=torch.uint8, device=dev)
-        self.block_table = torch.from_numpy(bt.astype(np.int32)).to(dev)
+        self.pool = torch.zeros((self.n_pages, N.PAGE_BYTES), dtype=torch.uint8,
+                                device=self.device)
+        # FS_DECODE_EARLY_PREFETCH: set by callers whose decode launches always
+        # follow a kernel that writes none of the tables / pages (the QKV GEMM
+        # in HybridDecodeRank); otherwise (K3 / K4 / restores just before) the
+        # launch reads nothing before its PDL wait
+        self.early_prefetch = False
+        self.fused = None  # (qoff, koff, voff) of the fused-qkv layout
+        self._install(work, bt.astype(np.int32))
+
+    def _seq_pages(self, item_req) -> np.ndarray:
+        """Pages backed per item: the full row, or the request's capacity."""
+        if self.request_capacity is None:
+            return np.full(len(item_req), self.pages_per_seq, dtype=np.int64)
+        if not len(item_req):
+            return np.zeros(0, np.int64)
+        return (self.request_capacity[item_req] + N.PAGE_TOKENS - 1) // N.PAGE_TOKENS
+
+    def _install(self, work: RankWork, bt: np.ndarray) -> None:
+        """(Re)build every device table of ``work`` over block table ``bt``."""
+        dev = self.device
+        n_seq = work.n_items
+        self.work = work
+        self.seq_tokens = self._seq_pages(work.item_req) * N.PAGE_TOKENS
+        self.block_table = torch.from_numpy(np.ascontiguousarray(bt, dtype=np.int32)).to(dev)
         self.item_seq = torch.arange(n_seq, dtype=torch.int32, device=dev)
         self.item_len = torch.zeros(n_seq, dtype=torch.int32, device=dev)
         self.item_pos = torch.zeros(n_seq, dtype=torch.int32, device=dev)
@@ -150,9 +194,8 @@ class PagedKVCache:
         # default ("blocks") layout: the query / output block of item i is
         # row request*n_slots + slot of a [B*n_slots, qpk, 128] tensor
         row = self._req * work.n_slots + self._slot
-        self.item_qoff = (row * q_per_kv * N.HEAD_DIM).to(torch.int32)
+        self.item_qoff = (row * self.qpk * N.HEAD_DIM).to(torch.int32)
         self.item_ooff = self.item_qoff
-        self.fused = None  # (qoff, koff, voff) of the fused-qkv layout
         self.seg_items = torch.from_numpy(work.seg_items).to(dev)
         self.page_off = torch.zeros(n_seq + work.num_layers, dtype=torch.int32, device=dev)
         seg = work.seg_items
@@ -160,9 +203,49 @@ class PagedKVCache:
         slots = N.lib.fs_decode_partial_slots(self.dev_index, self.max_items, -1)
         if slots < 0:
             raise SimulationError(f"cannot size decode partials: {N.lib.fs_last_error()}")
-        self.part_o = torch.empty((slots, q_per_kv, N.HEAD_DIM), dtype=torch.float32, device=dev)
-        self.part_lse = torch.empty((slots, q_per_kv), dtype=torch.float32, device=dev)
+        if getattr(self, "part_o", None) is None or self.part_o.shape[0] < slots:
+            self.part_o = torch.empty((slots, self.qpk, N.HEAD_DIM), dtype=torch.float32,
+                                      device=dev)
+            self.part_lse = torch.empty((slots, self.qpk), dtype=torch.float32, device=dev)
         self._descs = {}
+        if self.fused is not None:
+            self.set_fused_layout()
+
+    def adopt(self, work: RankWork):
+        """In-place adoption of a new work table (the on-demand shrink
+        target, recovery.py:396-427, with re-routed requests): items whose
+        (layer, head, request) this rank already serves keep their pages --
+        no KV moves; new items get pages from the free reserve; dropped
+        items return theirs.  Lengths must be set again afterwards.
+        Returns the indices (into the new work) of the new items, whose
+        pages the caller restores (K6) or recomputes."""
+        old_keys = item_keys(self.work)
+        new_keys = item_keys(work)
+        old_bt = self.block_table.cpu().numpy()
+        old_pages = self._seq_pages(self.work.item_req)
+        index = {k: i for i, k in enumerate(old_keys.tolist())}
+        kept = np.array([index.get(k, -1) for k in new_keys.tolist()], dtype=np.int64) \
+            if len(new_keys) else np.zeros(0, np.int64)
+        new_set = set(new_keys.tolist())
+        for i, k in enumerate(old_keys.tolist()):
+            if k not in new_set:  # dropped: its pages return to the reserve
+                self.free_pages.extend(int(x) for x in old_bt[i, :old_pages[i]])
+        need = self._seq_pages(work.item_req)
+        bt = np.zeros((work.n_items, self.pages_per_seq), dtype=np.int32)
+        fresh = np.flatnonzero(kept < 0)
+        if int(need[fresh].sum()) > len(self.free_pages):
+            raise SimulationError(
+                f"KV reserve exhausted: {int(need[fresh].sum())} pages needed, "
+                f"{len(self.free_pages)} free (raise reserve_pages)")
+        for i in range(work.n_items):
+            if kept[i] >= 0:
+                bt[i] = old_bt[kept[i]]
+            else:
+                n = int(need[i])
+                bt[i, :n] = self.free_pages[:n]
+                del self.free_pages[:n]
+        self._install(work, bt)
+        return fresh
 
     def set_fused_layout(self) -> int:
         """Use the fused projection layout: per request one row
@@ -230,7 +313,8 @@ class PagedKVCache:
 
     # -------------------------------------------------------------- decode --
     def _desc(self, layer, q, out, qkv, scale):
-        key = (layer, q.data_ptr(), out.data_ptr(), out.dtype, qkv, scale, self.config)
+        key = (layer, q.data_ptr(), out.data_ptr(), out.dtype, qkv, scale, self.config,
+               self.early_prefetch)
         d = self._descs.get(key)
         if d is not None:
             return d
@@ -264,6 +348,7 @@ class PagedKVCache:
         d.partial_slots = self.part_o.shape[0]
         d.device = self.dev_index
         d.config = self.config
+        d.flags = N.DECODE_EARLY_PREFETCH if self.early_prefetch else 0
         self._descs[key] = d
         return d
 

@@ -27,6 +27,21 @@ def test_library_exports_every_declared_symbol():
     assert N.lib.fs_abi_version() == 1
 
 
+def test_library_exports_nothing_undeclared():
+    """Every fs_* symbol the .so exports is declared in the header."""
+    import shutil
+    import subprocess
+    from paper_2511_14116_b200 import _native as N
+    nm = shutil.which("nm")
+    if nm is None:
+        pytest.skip("nm not available")
+    out = subprocess.run([nm, "-D", "--defined-only", N.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = sorted({ln.split()[-1] for ln in out.splitlines()
+                       if ln.split() and ln.split()[-1].startswith("fs_")})
+    assert exported == _declared()
+
+
 def test_native_placement_matches_golden(golden):
     from paper_2511_14116_b200.placement import make_placement, owner_array
     from paper_2511_14116_b200.core import ModelSpec
