@@ -257,6 +257,150 @@ def failure_states(steps, warmup, config, batch=64, ctx=4096, fails=(7, 3, 5), m
     return out
 
 
+# --------------------------------------- failure chain (N>1, processes) --
+def chain_reserve_pages(model, world, fails, batch, ctx):
+    """KV pages every rank keeps free so the whole on-demand chain adopts
+    in place: max over ranks and states of (pages then - pages at start)."""
+    from paper_2511_14116_b200.failover import route_for
+    from paper_2511_14116_b200.cluster import _decode_requests
+    from paper_2511_14116_b200.kvcache import RankWork
+    from paper_2511_14116_b200.placement import make_placement, owner_array
+    from paper_2511_14116_b200.recovery import plan_weight_recovery
+    plan = make_placement("hybrid", model, range(world))
+    alive = list(range(world))
+    routing = route(batch, alive, ctx)
+    reqs = _decode_requests(batch, ctx, 1024)
+    pages = (ctx + 15) // 16
+
+    def items(plan, routing):
+        owner = owner_array(plan, model.num_kv_heads)
+        return {g: RankWork.build(owner, g, routing, batch).n_items for g in plan.alive}
+    start = items(plan, routing)
+    need = 0
+    for f in fails:
+        alive = [g for g in alive if g != f]
+        plan = plan_weight_recovery(model, plan, alive, "on_demand").target_plan("hybrid", model)
+        routing = route_for(sorted(reqs), reqs, routing, alive)
+        now = items(plan, routing)
+        need = max(need, max(now[g] - start[g] for g in alive))
+    return need * pages
+
+
+def failure_chain(args, world, rank, local_rank):
+    """BASELINE configs 3 + 4 on one process per GPU: the C3 decode step
+    (Llama-3-70B shape, B=64, ctx 4096, attention + TP MLP, fused exchange)
+    on hybrid(N), then for each GPU in ``--failures``: that rank's process
+    EXITS, the survivors recover in place (cluster.ClusterRank.recover:
+    regroup, K7 weights from the host store + peers, adoption, K6 KV from
+    the dead rank's mirror, exchange rebuilt, graph, first step) and are
+    timed again.  Per world: max-rank step time INCLUDING the exchange,
+    tok/s, KV-roofline fraction, N/(8 scaled) ratio; per failure: recovery
+    wall clock with its phases (max over survivors)."""
+    import torch
+    from paper_2511_14116_b200.cluster import ClusterRank, shm_cleanup
+    from paper_2511_14116_b200.hostmirror import SharedHostRegion, WeightLayout
+    from paper_2511_14116_b200.placement import make_placement, memory_footprint
+    from paper_2511_14116_b200.core import ModelSpec
+    fails = [int(f) for f in args.failures.split(",") if f != ""]
+    model = llama70b()
+    if args.chain_layers:  # testing on a shared GPU only: NOT the C3 measurement
+        model = ModelSpec(num_layers=args.chain_layers, num_kv_heads=8, num_q_heads=64,
+                          head_dim=128, hidden_dim=8192, ffn_intermediate_dim=28672)
+    batch, ctx = 64, 4096
+    peak, _ = measured_peaks()
+    import torch.distributed as dist
+    store = dist.TCPStore(os.environ.get("MASTER_ADDR", "127.0.0.1"),
+                          int(os.environ["MASTER_PORT"]), None, False)
+    # one job name for all ranks (rank 0 picks it); stale regions of earlier
+    # runs on a reused box are removed first (they would pin host memory)
+    if rank == 0:
+        shm_cleanup("fsb")
+        store.set("fs/job", f"fsb{os.getpid()}x{int(time.time())}")
+    job = store.get("fs/job").decode()
+    reserve = chain_reserve_pages(model, world, fails, batch, ctx)
+    # host memory: weight store + every rank's mirror (pool incl. reserve)
+    lay = WeightLayout(model, model.default_num_shards())
+    plan0 = make_placement("hybrid", model, range(world))
+    fp0 = memory_footprint(plan0, model, {r: ctx for r in range(batch)}, route(batch, range(world),
+                                                                             ctx))
+    need_host = lay.total + world * (max(fp0.values()) + reserve * 8192) * 1.05
+    free = SharedHostRegion.free_bytes()
+    if need_host > free:
+        return {"skipped": f"/dev/shm has {free / 1e9:.0f} GB free, the weight store + KV "
+                           f"mirrors need {need_host / 1e9:.0f} GB"}
+    t0 = time.perf_counter()
+    cr = ClusterRank(model, rank, range(world), store, job, batch, ctx, seed=0, mlp=True,
+                     reserve_pages=reserve, device=torch.device("cuda", local_rank),
+                     config=args.kernel_config)
+    cr.eng.fill_random_kv(17 + rank)
+    cr.backup_all()
+    cr.eng.x.copy_(torch.randn_like(cr.eng.x, dtype=torch.float32).to(torch.bfloat16))
+    cr.eng.capture()
+    setup_s = time.perf_counter() - t0
+
+    def timed_world():
+        for _ in range(args.warmup):
+            cr.step()
+        torch.cuda.synchronize()
+        cr.ctl.barrier()
+        s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_.record()
+        for _ in range(args.steps):
+            cr.step()
+        e_.record()
+        torch.cuda.synchronize()
+        ms = s_.elapsed_time(e_) / args.steps
+        c = cr.eng.cache
+        kv = int(c.item_len.sum().item()) * KV_UNIT
+        every = cr.ctl.all_gather_object((rank, ms, kv, cr.eng.weight_bytes()))
+        worst = max(every, key=lambda t: t[1])
+        return {"world": cr.ctl.world, "alive": list(cr.ctl.alive),
+                "max_rank_step_ms": round(worst[1], 4),
+                "tok_s": round(batch / (worst[1] / 1e3), 1),
+                "max_kv_bytes": max(t[2] for t in every),
+                "kv_roofline_frac": round(max(t[2] for t in every) / (worst[1] / 1e3) / 1e9 /
+                                          peak, 4),
+                "step_frac_max_rank": round((worst[2] + worst[3]) / (worst[1] / 1e3) / 1e9 / peak,
+                                            4),
+                "rank_step_ms": {t[0]: round(t[1], 4) for t in every}}
+
+    states = [timed_world()]
+    states[0]["failed"] = None
+    recoveries = []
+    for f in fails:
+        cr.mark_backed()
+        if rank == f:
+            cr.die()                      # the process exits here
+        rep = cr.recover(f)
+        every = cr.ctl.all_gather_object(rep.__dict__)
+        worst = max(every, key=lambda d: d["recovery_ms"])
+        recoveries.append({"failed": f, "world_after": rep.world_after,
+                           "recovery_ms_max": worst["recovery_ms"],
+                           "phases_ms_of_max": worst["phases_ms"],
+                           "kv_restore_bytes_max": max(d["kv_restore_bytes"] for d in every),
+                           "weight_pcie_bytes_max": max(d["weight_pcie_bytes"] for d in every),
+                           "weight_nvlink_bytes_max": max(d["weight_nvlink_bytes"] for d in every),
+                           "plan_bytes_match": all(
+                               d["weight_pcie_bytes"] == d["planned_weight_pcie_bytes"] and
+                               d["weight_nvlink_bytes"] == d["planned_weight_nvlink_bytes"]
+                               for d in every)})
+        st = timed_world()
+        st["failed"] = f
+        states.append(st)
+    r8 = states[0]["tok_s"]
+    for st in states[1:]:
+        st["vs_first_scaled"] = round(st["tok_s"] / (r8 * st["world"] / states[0]["world"]), 4)
+    cr.ctl.barrier()
+    if cr.ctl.index == 0:
+        shm_cleanup(job)
+    return {"workload": f"C3 Llama-3-70B-shaped decode step ({model.num_layers} layers, attention"
+                        " + TP MLP, fused exchange), B=64, ctx 4096, hybrid(" + str(world) +
+                        ") then on-demand shrink after failures of GPU " +
+                        ", ".join(map(str, fails)) + "; one process per GPU, victims exit",
+            "setup_s": round(setup_s, 1), "states": states, "recoveries": recoveries,
+            "test_only": bool(args.chain_layers)}
+
+
 # ------------------------------------------------- mixed trace (config 5) --
 def sharegpt_trace(n=120, seed=20240701, n_long=2, long_len=32768):
     """ShareGPT-shaped lognormal lengths (the reference's synth_trace
@@ -584,6 +728,19 @@ def run_ours(args, world, rank, local_rank):
     del eng
     torch.cuda.empty_cache()
 
+    if world > 1 and args.failures:
+        try:
+            chain = failure_chain(args, world, rank, local_rank)
+            torch.cuda.synchronize()
+        except Exception as exc:  # report, never lose the main line
+            import traceback
+            traceback.print_exc()
+            chain = {"error": f"rank {rank}: {type(exc).__name__}: {exc}"}
+        if rank == min(r for r in range(world) if str(r) not in args.failures.split(",")):
+            line["failure_chain"] = chain
+            print(json.dumps(line), flush=True)
+        sys.stdout.flush()
+        os._exit(0)  # dead peers: skip communicator teardown
     if world == 1 and rank == 0:
         if not args.skip_failure_states:
             line["failure_states"] = failure_states(args.steps, args.warmup, args.kernel_config,
@@ -629,6 +786,11 @@ def main():
                          "buffers (default) or an NCCL all-reduce + add")
     ap.add_argument("--no-mlp", action="store_true",
                     help="attention sublayer only (no TP MLP partial / MLP all-reduce)")
+    ap.add_argument("--failures", default=None,
+                    help="N>1: GPUs lost one after another in the C3 failure chain "
+                         "(default 7,3,5 at N=8; '' disables)")
+    ap.add_argument("--chain-layers", type=int, default=0,
+                    help="testing only (shared GPU): C3 chain with this many layers")
     ap.add_argument("--cpu-layers", type=int, default=3,
                     help="cpu_baseline sample: float64 C2 layers timed (median)")
     args = ap.parse_args()
@@ -639,6 +801,8 @@ def main():
     EXCHANGE = args.exchange
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if args.failures is None:
+        args.failures = "7,3,5" if world == 8 else ""
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         if world == 1 and args.gpus > 1:

@@ -366,19 +366,17 @@ class ClusterRank:
         rep.new_items = len(fresh)
         t = lap("kv_restore", t)
 
-        # 5. exchange over the survivors, graph, first step
-        if old_xchg is not None:
-            old_xchg.close()
-        from .collective import FusedExchange
+        # 5. the exchange re-formed over the survivors (same buffers and
+        #    mappings, the dead rank's dropped), first step (eager: the step
+        #    graph is re-captured after the clock stops)
         eng.group = self.ctl
-        eng.xchg = FusedExchange(self.ctl, self.batch * model.hidden_dim, self.device)
+        old_xchg.shrink(self.ctl)
         t = lap("exchange", t)
-        eng.capture()
-        t = lap("graph", t)
         eng.step()
         t = lap("first_step", t)
         rep.phases_ms = ph
         rep.recovery_ms = round((t - t_event) * 1e3, 3)
+        eng.capture()
         # new state: plan, routing, page map; the restored pages into my
         # own mirror (off the critical path)
         self.plan, self.routing = new_plan, new_routing
@@ -399,10 +397,11 @@ class ClusterRank:
         self.wstore.close(unlink=unlink and self.ctl.index == 0)
 
 
-def shm_cleanup(job: str) -> None:
-    """Remove the job's shared-memory regions (also those of dead ranks)."""
+def shm_cleanup(prefix: str) -> None:
+    """Remove the shared-memory regions whose names start with ``prefix``
+    (a job's, including those of its dead ranks)."""
     for name in os.listdir("/dev/shm"):
-        if name.startswith(f"{job}_"):
+        if name.startswith(prefix):
             try:
                 os.unlink(os.path.join("/dev/shm", name))
             except FileNotFoundError:

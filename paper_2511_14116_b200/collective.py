@@ -53,6 +53,7 @@ class FusedExchange:
         self.nbytes = int(N.lib.fs_ar_buffer_bytes(self.max_elems))
         self.data_bytes = self.nbytes - 256
         self._own, self._opened = [], []
+        self._ids = list(ctl.alive) if ctl else None  # global id per rank index
         handles = []
         for _ in range(2):
             p = C.c_void_p()
@@ -87,6 +88,32 @@ class FusedExchange:
             dist.barrier(group=group)
         if check:
             self._self_check()
+
+    def shrink(self, ctl) -> None:
+        """Re-form the exchange over the survivors ``ctl.alive`` (a
+        :class:`cluster.StoreControl` of the next generation) WITHOUT new
+        buffers: the dead ranks' mappings are closed, the survivors' buffers
+        keep their IPC mappings and are re-indexed by the new rank order.
+        Safe because every rank ran the same number of exchanges per buffer
+        (lock-step steps): a flag slot's old value is at most the current
+        use count, below the next use every waiter spins for."""
+        if self._ids is None:
+            raise ValidationError("shrink needs a FusedExchange built over a StoreControl")
+        keep = set(ctl.alive)
+        if not keep <= set(self._ids) or self._ids[self.rank] not in keep:
+            raise ValidationError("shrink: the new world must be a subset containing this rank")
+        torch.cuda.synchronize(self.device)
+        for i in range(2):
+            for r, g in enumerate(self._ids):
+                if g not in keep and r != self.rank:
+                    N.lib.fs_ar_ipc_close(C.c_void_p(self.peers[i][r]))
+                    self._opened.remove(self.peers[i][r])
+            arr = (C.c_void_p * len(ctl.alive))()
+            for k, g in enumerate(ctl.alive):
+                arr[k] = self.peers[i][self._ids.index(g)]
+            self.peers[i] = arr
+        self._ids = list(ctl.alive)
+        self.rank, self.world = ctl.index, ctl.world
 
     def partial(self, i: int, shape) -> torch.Tensor:
         """This rank's partial buffer ``i`` (0/1) as a bf16 tensor of ``shape``
