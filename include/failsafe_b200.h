@@ -80,10 +80,10 @@ extern "C" {
  * K rows [0,16) then V rows [0,16).  Each half is two 2 KB atoms (head
  * dims 0-63, then 64-127); an atom is 16 rows x 128 B with the 16-byte chunk
  * c (0..7) of row r stored at chunk position c ^ (r & 7) -- the tcgen05 /
- * TMA SWIZZLE_128B pattern, and bank-conflict-free for ldmatrix.  K is
- * bf16; V is stored as f16 (fs_kv_write converts: exact for bf16 values
- * with |v| in [2^-14, 65504], saturating beyond), so P.V runs with f16
- * probabilities.  8 KiB per page. */
+ * TMA SWIZZLE_128B pattern, and bank-conflict-free for ldmatrix.  K and
+ * V are bf16, stored exactly as given (any finite bf16 value round-trips);
+ * the kernels run P.V with P split into a bf16 hi + lo pair.  8 KiB per
+ * page. */
 #define FS_PAGE_TOKENS 16
 #define FS_HEAD_DIM 128
 #define FS_PAGE_BYTES 8192
@@ -208,8 +208,8 @@ typedef struct fs_prefill_desc {
     int32_t n_comb;
     int32_t q_per_kv;          /* 1..8                                      */
     float scale;
-    void *part_o;              /* [partial_slots][rows][128] f16 (split
-                                  partials O / l; bounded by max |V|)       */
+    void *part_o;              /* [partial_slots][rows][128] fp32 (split
+                                  partials O / l)                           */
     float *part_lse;           /* [partial_slots][rows]                     */
     int64_t partial_slots;
     int32_t variant;           /* 0: tcgen05 (TMEM accumulators, 256-row

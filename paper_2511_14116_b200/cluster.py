@@ -166,6 +166,7 @@ class ClusterRank:
         # a multi-GB mapping is slow; the failure path must not pay it)
         self.peer_mirrors = {g: KVMirror(f"{job}_kv{g}") for g in self.ctl.alive if g != rank}
         self.reports = []
+        self.ctl.barrier()  # the next exchange spins on every rank: leave together
 
     # ------------------------------------------------------------ serving --
     def _initial_routing(self):
@@ -217,8 +218,22 @@ class ClusterRank:
         os._exit(0)
 
     # ----------------------------------------------------------- recovery --
+    def wait_dead(self, failed: int, timeout_s: float = 300.0) -> float:
+        """Failure detection: block until ``failed`` posted its loss (the
+        injected failure's notice; its mirror is final from then on).
+        Returns the posted wall time."""
+        key = f"fs/dead/{failed}"
+        t0 = time.monotonic()
+        while not self.ctl.store.check([key]):
+            if time.monotonic() - t0 > timeout_s:
+                raise SimulationError(f"rank {failed} never reported its loss")
+            time.sleep(0.0002)
+        return float(self.ctl.store.get(key).decode())
+
     def recover(self, failed: int) -> RecoveryReport:
-        """Run on every survivor at the failure event (see module doc)."""
+        """Run on every survivor at the failure event (see module doc):
+        the clock starts when the loss is detected (the dead rank's notice)."""
+        self.wait_dead(failed)
         t_event = time.perf_counter()
         ph = {}
 
@@ -371,6 +386,7 @@ class ClusterRank:
         #    graph is re-captured after the clock stops)
         eng.group = self.ctl
         old_xchg.shrink(self.ctl)
+        self.ctl.barrier()  # the first exchange spins on every survivor: start together
         t = lap("exchange", t)
         eng.step()
         t = lap("first_step", t)
@@ -385,6 +401,7 @@ class ClusterRank:
             m.close()
         self._publish_tables()
         self.backup_all()
+        self.ctl.barrier()  # every survivor's mirror is consistent before serving resumes
         self.reports.append(rep)
         return rep
 

@@ -15,7 +15,7 @@
 // its exchange on buffer B passed its barrier, i.e. after every peer
 // finished reading A.  The use counter and flags live in device memory, so
 // the launch is CUDA-graph capturable.  A peer that never arrives makes the
-// kernel trap after 5 s instead of hanging the GPU.
+// kernel trap after 20 s instead of hanging the GPU.
 #include <cuda_bf16.h>
 
 #include <cstring>
@@ -24,7 +24,7 @@
 
 namespace fs {
 
-constexpr int64_t kSpinNs = 5000000000LL;  // 5 s
+constexpr int64_t kSpinNs = 20000000000LL;  // 20 s
 
 struct ArParams {
     uint8_t *peer[FS_AR_MAX_WORLD];

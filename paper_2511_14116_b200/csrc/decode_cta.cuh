@@ -151,7 +151,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_cta_kernel(const DecodeP
                     const uint32_t r = (len - 1) % kPageTokens, ch = lane & 15, half = lane >> 4;
                     const int64_t src = (half ? p.item_voff[item] : p.item_koff[item]) + ch * 8;
                     uint4 v = *reinterpret_cast<const uint4 *>(p.kv_new + src);
-                if (half) v = bf16x8_to_f16x8(v);  // V pages hold f16
                     const uint32_t ofs = half * kHalfPage + swz(r, ch);
                     *reinterpret_cast<uint4 *>(page_s + ofs) = v;
                     const int64_t pg = p.bt[(int64_t)p.item_seq[item] * p.bt_stride + pidx];
@@ -199,9 +198,14 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_cta_kernel(const DecodeP
                 o[mt][2] *= al0;
                 o[mt][3] *= al1;
             }
-            // P^T in f16 (11 mantissa bits) against the f16 V pages: bf16 P would cost
-            // ~1.5e-3 mean relative error on long contexts (north star: 1e-3)
-            const uint32_t pb0 = movmatrix_t(pack_f16(p0, p1)), pb1 = movmatrix_t(pack_f16(p2, p3));
+            // P^T as a bf16 hi + lo pair (~16 mantissa bits) against the bf16 V
+            // pages: two bf16 MMAs per V block (bf16 P alone costs ~1.5e-3 mean
+            // relative error on long contexts; north star: 1e-3)
+            uint32_t h01, l01, h23, l23;
+            split_bf16x2(p0, p1, h01, l01);
+            split_bf16x2(p2, p3, h23, l23);
+            const uint32_t pb0 = movmatrix_t(h01), pb1 = movmatrix_t(h23);
+            const uint32_t pl0 = movmatrix_t(l01), pl1 = movmatrix_t(l23);
             {
                 const int i = lane >> 3;
                 const uint32_t r = (lane & 7) + ((i >> 1) << 3);
@@ -209,7 +213,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_cta_kernel(const DecodeP
                 for (int mt = 0; mt < 8; ++mt) {
                     uint32_t a0, a1, a2, a3;
                     ldsm_x4_t(vb + swz(r, 2 * mt + (i & 1)), a0, a1, a2, a3);
-                    mma_f16(o[mt], a0, a1, a2, a3, pb0, pb1);
+                    mma_bf16(o[mt], a0, a1, a2, a3, pb0, pb1);
+                    mma_bf16(o[mt], a0, a1, a2, a3, pl0, pl1);
                 }
             }
             __syncwarp();

@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(256) kv_write_kernel(uint8_t *pool, const int3
     const uint8_t *src = (half ? v_src : k_src) + (int64_t)tok_src[t] * src_stride_bytes + c * 16;
     uint8_t *dst = pool + page * kPageBytes + half * kHalfPage + swz(r, c);
     const uint4 v = *reinterpret_cast<const uint4 *>(src);
-    *reinterpret_cast<uint4 *>(dst) = half ? bf16x8_to_f16x8(v) : v;  // V pages hold f16
+    *reinterpret_cast<uint4 *>(dst) = v;
 }
 
 // K3 over token runs: warp = token; the run is found by a binary search of
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(256) kv_write_runs_kernel(
                          ((int64_t)run_src[lo] + (int64_t)i * src_step) * src_stride_bytes + c * 16;
     uint8_t *dst = pool + page * kPageBytes + half * kHalfPage + swz(r, c);
     const uint4 v = *reinterpret_cast<const uint4 *>(src);
-    *reinterpret_cast<uint4 *>(dst) = half ? bf16x8_to_f16x8(v) : v;  // V pages hold f16
+    *reinterpret_cast<uint4 *>(dst) = v;
 }
 
 __global__ void __launch_bounds__(256) kv_read_kernel(const uint8_t *pool, const int32_t *bt,
@@ -70,14 +70,7 @@ __global__ void __launch_bounds__(256) kv_read_kernel(const uint8_t *pool, const
     const uint32_t r = pos % kPageTokens, c = lane & 15, half = lane >> 4;
     uint8_t *dst = (half ? v_dst : k_dst) + (int64_t)tok_dst[t] * dst_stride_bytes + c * 16;
     const uint8_t *src = pool + page * kPageBytes + half * kHalfPage + swz(r, c);
-    uint4 v = *reinterpret_cast<const uint4 *>(src);
-    if (half) {
-        v.x = f16x2_to_bf16x2(v.x);
-        v.y = f16x2_to_bf16x2(v.y);
-        v.z = f16x2_to_bf16x2(v.z);
-        v.w = f16x2_to_bf16x2(v.w);
-    }
-    *reinterpret_cast<uint4 *>(dst) = v;
+    *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<const uint4 *>(src);
 }
 
 // K5/K6: page-granular gather (pool -> contiguous) / scatter (contiguous ->

@@ -15,10 +15,9 @@
 // pages that straddle the tile's diagonal.  The page layout (swizzled 16 B
 // chunks) is the one the decode kernel and the writers share.
 //
-// P.V runs in f16, not bf16: V pages are stored in f16 (exact for the bf16
-// values the projections produce, |v| <= 65504), so the probabilities keep
-// 11 mantissa bits -- bf16 P alone costs ~1.5e-3 mean relative error on long
-// contexts, above the 1e-3 the north star allows.  The producer warps zero
+// P.V: P is split into a bf16 hi + lo pair (~16 mantissa bits) against the
+// bf16 V pages -- two MMAs; bf16 P alone costs ~1.5e-3 mean relative error
+// on long contexts, above the 1e-3 the north star allows.  The producer warps zero
 // stale rows past an item's last token and publish each page on a third
 // barrier.
 //
@@ -55,7 +54,7 @@ struct PrefillParams {
     int32_t qpk, tpt;  // q heads per kv head, chunk tokens per tile
     int32_t rows;      // query rows per tile (= partial rows per slot): 64 or 128
     float scale_log2;
-    __half *part_o;     // split partials O / l: f16 (|O| <= max|V|, f16 V pages)
+    float *part_o;      // split partials O / l (fp32)
     float *part_lse;
 };
 
@@ -85,8 +84,8 @@ __global__ void __launch_bounds__((kConsumerWarps + 2) * 32) prefill_kernel(cons
     if (warp >= kConsumerWarps) {
         // ---- producer warps: warp 4 issues the TMA ring (refilling the
         // stage released two pages ago, so the refill never waits on the
-        // page being computed); warps 4 and 5 each convert half of every
-        // landed V half-page to f16 in place and arrive on `ready` ----
+        // page being computed); warps 4 and 5 each zero the stale rows of
+        // half of every landed V half-page and arrive on `ready` ----
         const int cw = warp - kConsumerWarps;
         const int64_t row = (int64_t)p.item_seq[item] * p.bt_stride + pg0;
         const int kv_end = p.item_start[item] + p.item_len[item];
@@ -120,7 +119,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 2) * 32) prefill_kernel(cons
             mbar_wait(full0 + 8 * s, (k / STAGES) & 1);
             // rows past the item's last written position may hold stale
             // bytes: zero them in this warp's atom (their P is 0, but 0 *
-            // NaN/Inf is not); V is already f16 in the pages
+            // NaN/Inf is not)
             const int rows_ok = kv_end - (pg0 + k) * kPageTokens;
             if (rows_ok < kPageTokens) {
                 uint4 *vh = reinterpret_cast<uint4 *>(smem + s * kPageBytes + kHalfPage +
@@ -230,14 +229,20 @@ __global__ void __launch_bounds__((kConsumerWarps + 2) * 32) prefill_kernel(cons
             o[nt][2] *= ab;
             o[nt][3] *= ab;
         }
-        const uint32_t a0 = pack_f16(sc[0][0], sc[0][1]), a1 = pack_f16(sc[0][2], sc[0][3]);
-        const uint32_t a2 = pack_f16(sc[1][0], sc[1][1]), a3 = pack_f16(sc[1][2], sc[1][3]);
+        // P as a bf16 hi + lo pair against the bf16 V page (two MMAs)
+        uint32_t a0, a1, a2, a3, e0, e1, e2, e3;
+        split_bf16x2(sc[0][0], sc[0][1], a0, e0);
+        split_bf16x2(sc[0][2], sc[0][3], a1, e1);
+        split_bf16x2(sc[1][0], sc[1][1], a2, e2);
+        split_bf16x2(sc[1][2], sc[1][3], a3, e3);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             uint32_t b0, b1, b2, b3;
             ldsm_x4_t(vbuf + swz(vrow, 2 * j + vch), b0, b1, b2, b3);
-            mma_f16(o[2 * j], a0, a1, a2, a3, b0, b1);
-            mma_f16(o[2 * j + 1], a0, a1, a2, a3, b2, b3);
+            mma_bf16(o[2 * j], a0, a1, a2, a3, b0, b1);
+            mma_bf16(o[2 * j + 1], a0, a1, a2, a3, b2, b3);
+            mma_bf16(o[2 * j], e0, e1, e2, e3, b0, b1);
+            mma_bf16(o[2 * j + 1], e0, e1, e2, e3, b2, b3);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive_cta(empty0 + 8 * s);
@@ -270,12 +275,12 @@ __global__ void __launch_bounds__((kConsumerWarps + 2) * 32) prefill_kernel(cons
             }
         }
     } else {
-        __half *po = p.part_o + (int64_t)slot * kTileRows * kHeadDim;
+        float *po = p.part_o + (int64_t)slot * kTileRows * kHeadDim;
 #pragma unroll
         for (int nt = 0; nt < 16; ++nt) {
             const int d = nt * 8 + 2 * tig;
-            *reinterpret_cast<uint32_t *>(po + ra * kHeadDim + d) = pack_f16_sat(o[nt][0] * ia, o[nt][1] * ia);
-            *reinterpret_cast<uint32_t *>(po + rb * kHeadDim + d) = pack_f16_sat(o[nt][2] * ib, o[nt][3] * ib);
+            *reinterpret_cast<float2 *>(po + ra * kHeadDim + d) = make_float2(o[nt][0] * ia, o[nt][1] * ia);
+            *reinterpret_cast<float2 *>(po + rb * kHeadDim + d) = make_float2(o[nt][2] * ib, o[nt][3] * ib);
         }
         if (tig == 0) {
             p.part_lse[(int64_t)slot * kTileRows + ra] = la > 0.f ? ma + __log2f(la) : -INFINITY;
@@ -314,33 +319,36 @@ __global__ void __launch_bounds__(256) prefill_combine_kernel(const PrefillParam
 #pragma unroll
         for (int i = 0; i < 8; ++i) mx = fmaxf(mx, v[i]);
     }
-    const uint4 *po = reinterpret_cast<const uint4 *>(p.part_o + ((int64_t)slot0 * p.rows + r) * kHeadDim) + c;
-    const int64_t sstr = (int64_t)p.rows * (kHeadDim / 8);  // 16-B chunks per split slot
+    // this thread's 8 dims of every split: two float4 per split slot
+    const float4 *po = reinterpret_cast<const float4 *>(p.part_o + ((int64_t)slot0 * p.rows + r) * kHeadDim) + 2 * c;
+    const int64_t sstr = (int64_t)p.rows * (kHeadDim / 4);  // float4s per split slot
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     float den = 0.f;
     for (int s0 = 0; s0 < ns; s0 += 4) {
         float w[4];
-        uint4 vv[4];
+        float4 va[4], vb[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             w[i] = 0.f;
-            vv[i] = make_uint4(0, 0, 0, 0);
+            va[i] = vb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (s0 + i < ns) {
                 const float l = __ldg(lse + (int64_t)(s0 + i) * p.rows);
                 w[i] = l == -INFINITY ? 0.f : fast_exp2(l - mx);
-                vv[i] = __ldg(po + (s0 + i) * sstr);
+                va[i] = __ldg(po + (s0 + i) * sstr);
+                vb[i] = __ldg(po + (s0 + i) * sstr + 1);
             }
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             den += w[i];
-            const uint32_t hw[4] = {vv[i].x, vv[i].y, vv[i].z, vv[i].w};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&hw[k]));
-                acc[2 * k] += w[i] * f.x;
-                acc[2 * k + 1] += w[i] * f.y;
-            }
+            acc[0] += w[i] * va[i].x;
+            acc[1] += w[i] * va[i].y;
+            acc[2] += w[i] * va[i].z;
+            acc[3] += w[i] * va[i].w;
+            acc[4] += w[i] * vb[i].x;
+            acc[5] += w[i] * vb[i].y;
+            acc[6] += w[i] * vb[i].z;
+            acc[7] += w[i] * vb[i].w;
         }
     }
     const float inv = den > 0.f ? 1.f / den : 0.f;
@@ -522,7 +530,7 @@ extern "C" int fs_prefill_attention(const fs_prefill_desc *d, void *stream) {
     prm.rows = variant_rows(d->variant);
     prm.tpt = prm.rows / d->q_per_kv;
     prm.scale_log2 = d->scale * 1.4426950408889634f;
-    prm.part_o = static_cast<__half *>(d->part_o);
+    prm.part_o = static_cast<float *>(d->part_o);
     prm.part_lse = d->part_lse;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     static bool attr_set[4][64] = {{false}};

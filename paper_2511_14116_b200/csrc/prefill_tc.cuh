@@ -9,8 +9,8 @@
 // one half is in softmax (FA4's two-tile ping-pong).  KV is consumed in
 // blocks of 64 keys (4 pages).  Per block j and half h:
 //     S_j[128 x 64]   = Q[128 x 128] . K_j^T     tcgen05.mma, bf16, -> TMEM
-//     P_j             = exp2(S_j*scale - m)       softmax warps, f16 -> TMEM
-//     O[128 x 128]   += P_j . V_j                 tcgen05.mma, f16, TMEM acc
+//     P_j             = exp2(S_j*scale - m)       softmax warps, bf16 hi + lo -> TMEM
+//     O[128 x 128]   += P_j . V_j                 2 x tcgen05.mma (hi, lo), bf16, TMEM acc
 // Roles (NQ*128 + 64 threads): warps 0..4NQ-1 = softmax / correction /
 // epilogue (thread = row = TMEM lane; half h = warp / 4), warp 4NQ = TMA
 // producer (each page = 4 bulk copies of
@@ -18,10 +18,12 @@
 // K as the K-major B of S, V as the MN-major B of P.V), warp 5 = MMA issuer
 // (one thread) + TMEM owner.  S is double-buffered in TMEM so S_{j+2} is
 // computed while the softmax warps work on S_{j+1}; the softmax warps store
-// P (f16) over S_j's columns and P.V_j reads its A operand from TMEM (no
+// P (bf16 hi | lo halves) over S_j's columns and P.V_j reads its A operands from TMEM (no
 // shared-memory round trip).  The running max is rescaled lazily (FA4): O and l are only
-// rescaled when a row's max grows by more than 2^8, so P <= 256 stays exact
-// in f16 and most blocks never touch O.
+// rescaled when a row's max grows by more than 2^8 (P <= 256) and most
+// blocks never touch O.  P is split into bf16 hi + lo (~16 mantissa bits;
+// bf16 P alone costs ~1.5e-3 mean relative error at 4k context, over the
+// north star's 1e-3) against the bf16 V pages, so P.V is two MMAs.
 //
 // TMEM (half h at column 256h): O at [0, 128), S buffers at [128, 192) and
 // [192, 256).
@@ -42,14 +44,14 @@ constexpr int tc_smem() {
 constexpr float kTcRescale = 8.f;                 // lazy-rescale threshold (log2)
 
 // kind::f16 instruction descriptors: D fp32; S: A = Q bf16 K-major, B = K
-// bf16 K-major, M 128, N 64; PV: A = P f16 K-major, B = V f16 MN-major,
+// bf16 K-major, M 128, N 64; PV: A = P bf16 K-major, B = V bf16 MN-major,
 // M 128, N 128
 template <int BK>
 constexpr uint32_t tc_idesc_s() {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BK >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
 }
-constexpr uint32_t kIdescPV = (1u << 4) | (1u << 16) | ((uint32_t)(kHeadDim >> 3) << 17) |
-                              ((uint32_t)(kTcRows >> 4) << 24);
+constexpr uint32_t kIdescPV = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
+                              ((uint32_t)(kHeadDim >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
 
 __device__ __forceinline__ uint64_t tc_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
     uint64_t d = 0;
@@ -359,6 +361,7 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
                     for (int k = 0; k < kTcKeys / 16; ++k) {
                         const uint64_t bd = tc_desc(vs + k * 2048, kAtom, 1024);
                         tc_mma_f16_ta(tmem + 256 * h, pt + k * 8, bd, kIdescPV, (j > 0 || k > 0) ? 1u : 0u);
+                        tc_mma_f16_ta(tmem + 256 * h, pt + kTcKeys / 2 + k * 8, bd, kIdescPV, 1u);
                     }
                     tc_commit_bar(o_done + 8 * (2 * h + b));
                 }
@@ -464,13 +467,14 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
             const float mu = m_used == -INFINITY ? 0.f : m_used;
             uint64_t ls2[2] = {f2(0.f, 0.f), f2(0.f, 0.f)};
             const uint64_t scale2 = f2(scale, scale), nmu2 = f2(-mu, -mu);
-            // P_j (f16, 2 keys per 32-bit column) over the S_j columns in
+            // P_j (bf16 hi in the first half of the S_j columns, lo in the
+            // second; 2 keys per 32-bit column) over the S_j columns in
             // TMEM: the A operand of P.V_j; one 32-column S group -> 16
             // packed P columns at a time, so each group's registers die as
             // soon as it is stored
 #pragma unroll
             for (int hh = 0; hh < kC; ++hh) {
-                uint32_t pk[16];
+                uint32_t pk[16], pl[16];
 #pragma unroll
                 for (int c = 0; c < 16; ++c) {
                     float x0, x1;
@@ -485,9 +489,10 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
                     }
                     const uint64_t e2 = f2(e0, e1);
                     ls2[c & 1] = fadd2(ls2[c & 1], e2);
-                    pk[c] = pack_f16(e0, e1);
+                    split_bf16x2(e0, e1, pk[c], pl[c]);
                 }
                 tc_st16(s_t + b * kTcKeys + 16 * hh, pk);
+                tc_st16(s_t + b * kTcKeys + kTcKeys / 2 + 16 * hh, pl);
             }
             tc_wait_st();
             float ls[4];
@@ -548,11 +553,8 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
         for (int rr = 0; rr < 32; ++rr) {
             const float4 v = reinterpret_cast<const float4 *>(stg + rr * kHeadDim)[lane ^ (rr & 7)];
             const int Rr = wrow0 + rr;
-            if (slot >= 0) {  // f16 partial: 4 dims = 8 B per lane
-                uint2 hv;
-                hv.x = pack_f16_sat(v.x, v.y);
-                hv.y = pack_f16_sat(v.z, v.w);
-                reinterpret_cast<uint2 *>(p.part_o + ((int64_t)slot * rows + Rr) * kHeadDim)[lane] = hv;
+            if (slot >= 0) {  // fp32 partial: 4 dims = 16 B per lane
+                reinterpret_cast<float4 *>(p.part_o + ((int64_t)slot * rows + Rr) * kHeadDim)[lane] = v;
                 continue;
             }
             const int tk = tok0 + Rr / qpk;

@@ -136,7 +136,7 @@ class PrefillLaunch:
             tab = torch.from_numpy(self.host_table).to(cache.device)
             po = pl = None
             if self.n_slots:
-                po = torch.empty((self.n_slots, tp.rows, N.HEAD_DIM), dtype=torch.float16,
+                po = torch.empty((self.n_slots, tp.rows, N.HEAD_DIM), dtype=torch.float32,
                                  device=cache.device)
                 pl = torch.empty((self.n_slots, tp.rows), dtype=torch.float32,
                                  device=cache.device)

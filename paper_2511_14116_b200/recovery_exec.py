@@ -162,8 +162,11 @@ def recovery_microbench(batch: int = 64, ctx: int = 4096, fails=(7, 3, 5)) -> di
     n_gpus = torch.cuda.device_count()
     plan = make_placement("hybrid", model, range(8))
     alive = list(range(8))
+    from .cluster import _decode_requests
+    from .failover import route_for
     contexts = {r: ctx for r in range(batch)}
     routing = {r: r % 8 for r in range(batch)}
+    requests = _decode_requests(batch, ctx, 1024)
     backup = BackupState(host_memory_bytes=2 * 10 ** 12,
                          kv_bytes_per_token=model.kv_bytes_per_token())
     for r in range(batch):
@@ -176,15 +179,17 @@ def recovery_microbench(batch: int = 64, ctx: int = 4096, fails=(7, 3, 5)) -> di
         new_alive = [g for g in alive if g != f]
         wp = plan_weight_recovery(model, plan, new_alive, "on_demand")
         new_plan = wp.target_plan("hybrid", model)
-        new_routing = {r: new_alive[r % len(new_alive)] for r in range(batch)}
+        # requests keep their rank when it survives (simulation.py:376-388)
+        new_routing = route_for(sorted(requests), requests, routing, new_alive)
         kp = plan_kv_recovery(backup, plan, new_plan, model, contexts, routing, new_routing,
                               "host_restore")
         kv_by = kp.pcie_bytes_by_gpu()
+        kv_nvl = kp.nvlink_bytes_by_gpu()
         w_pcie, w_nvl = wp.pcie_bytes_by_gpu(), wp.nvlink_bytes_by_gpu()
         g_kv = max(kv_by, key=kv_by.get)
         g_w = max(w_pcie, key=w_pcie.get)
-        plans.append((f, len(new_alive), kv_by[g_kv], w_pcie[g_w], max(w_nvl.values()),
-                      kp.recompute_tokens))
+        plans.append((f, len(new_alive), kv_by[g_kv], w_pcie[g_w],
+                      max(w_nvl.values()) + max(kv_nvl.values() or [0]), kp.recompute_tokens))
         max_bytes = max(max_bytes, kv_by[g_kv], w_pcie[g_w])
         plan, alive, routing = new_plan, new_alive, new_routing
 
@@ -233,7 +238,7 @@ def recovery_microbench(batch: int = 64, ctx: int = 4096, fails=(7, 3, 5)) -> di
                       "weight_pcie_bytes_max_gpu": w_pcie, "weight_h2d_ms": round(w_ms, 3),
                       "weight_nvlink_bytes_max_gpu": w_nvl, "weight_p2p_ms": round(p_ms, 3),
                       "weight_p2p_kind": p_kind, "recompute_requests": len(recompute),
-                      "recovery_ms": round(total, 3)})
+                      "recovery_ms_assembled": round(total, 3)})
     # K5: backup gather throughput and per-step volume
     n_bk = min(max_bytes // N.PAGE_BYTES, 131072)
     pool = dev_buf[: n_bk * N.PAGE_BYTES].view(n_bk, N.PAGE_BYTES)
@@ -254,5 +259,8 @@ def recovery_microbench(batch: int = 64, ctx: int = 4096, fails=(7, 3, 5)) -> di
             "backup_gather_gbs": round(n_bk * N.PAGE_BYTES / g_ms / 1e6, 1),
             "backup_pages_per_decode_step_n8": new_pages_per_step,
             "backup_bytes_per_decode_step_n8": int(new_pages_per_step * N.PAGE_BYTES),
-            "note": "KV restore = K6 scatter from pinned host (PCIe); weights = reference "
-                    "on-demand plan bytes for the heaviest survivor"}
+            "note": "ASSEMBLED, not end to end: isolated K6 / H2D copy timings of the plans' "
+                    "bytes for the heaviest survivor plus the NVLink part (weights + KV "
+                    "nvlink_peer) measured with a peer GPU or modeled at 770 GB/s; routing "
+                    "by route_for.  The end-to-end recovery wall clock (processes, "
+                    "regroup, adoption, first step) is bench.py --gpus N's failure_chain"}

@@ -158,7 +158,7 @@ class StepPlan:
             o += size
         slots = max([lp.n_slots for lp in self.prefill if lp is not None] + [0])
         rows = max([lp.plan.rows for lp in self.prefill if lp is not None] + [64])
-        self.pf_part_o = torch.empty((max(1, slots), rows, hd), dtype=torch.float16, device=dev)
+        self.pf_part_o = torch.empty((max(1, slots), rows, hd), dtype=torch.float32, device=dev)
         self.pf_part_lse = torch.empty((max(1, slots), rows), dtype=torch.float32, device=dev)
         o = pf_base
         for lp in self.prefill:

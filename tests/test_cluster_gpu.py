@@ -124,8 +124,9 @@ def test_processes_lose_ranks_and_resume_bit_exact(tmp_path, world, fails):
                 p.kill()
         from paper_2511_14116_b200.cluster import shm_cleanup
         shm_cleanup(job)
-    for r, p in enumerate(procs):
-        assert p.returncode == 0, f"rank {r} failed:\n{logs[r][-3000:]}"
+    bad = [r for r, p in enumerate(procs) if p.returncode != 0]
+    assert not bad, "\n".join(f"rank {r} (rc {procs[r].returncode}):\n{logs[r][-2500:]}"
+                               for r in bad)
     del store
     exp = _emulated(world, fails, steps_before, batch, ctx)
     alive = list(range(world))
