@@ -465,12 +465,112 @@ def gen_decode():
     return {"head_dim": hd, "cases": cases}
 
 
+def gen_reconfig():
+    """Reconfiguration decisions of the live reference's serving loop
+    (simulation.py:198-397): a Simulation over the bundled mooncake_small
+    trace with a fail / fail / recover failure CSV, and a small-HBM cluster
+    whose second shrink preempts residents.  For every reconfiguration the
+    inputs at ``_reconfigure`` (alive set, plan tables, residents with their
+    progress, routing, backup watermarks) and the outcome after
+    ``_handle_reconfig_done`` (serving world, target plan, routing, residents
+    / waiting order, preempted ids, capacities, reservations, router
+    workload) are recorded by wrapping the two methods on the instance (the
+    reference code is not modified).  With preemption the reference's run
+    stops at its next iteration (KeyError: the preempted request stays in
+    the rebuilt router's prefill queue, simulation.py:255-262 vs 458-462);
+    the recorded decisions precede that."""
+    import dataclasses
+    from failsafe.costmodel import CostParams
+    from failsafe.recovery import load_failure_trace
+    from failsafe.simulation import SimConfig, Simulation
+    from failsafe.traces import load_request_trace
+    model, cluster = load_config(os.path.join(DATA, "llama70b.toml"))
+    with open(os.path.join(DATA, "traces", "mooncake_small.csv")) as fh:
+        rows = load_request_trace(fh.read())[:40]
+    H = model.num_kv_heads
+
+    def req_state(sim, rid):
+        r = sim.requests[rid]
+        return [rid, r.arrival_time, r.input_len, r.output_len, r.tokens_prefilled,
+                r.tokens_decoded]
+
+    scenarios = []
+    for name, hbm, csv in (("expand", 80_000_000_000,
+                            "10.0,fail,7\n20.0,fail,3\n35.0,recover,7\n"),
+                           ("preempt", 32_000_000_000,
+                            "10.0,fail,7\n20.0,fail,3\n35.0,recover,7\n")):
+        cl = dataclasses.replace(cluster, hbm_bytes_per_gpu=hbm, switch_latency=0.5)
+        fails = load_failure_trace("ts_s,event,gpu_id\n" + csv)
+        sim = Simulation(model, cl, CostParams.from_model(model), SimConfig(max_time=60.0),
+                         rows, fails)
+        events = []
+        orig_reconf, orig_done, orig_preempt = (sim._reconfigure, sim._handle_reconfig_done,
+                                                sim._preempt)
+        preempted = []
+
+        def reconf():
+            if sim.plan is None or sim._desired_serving() is None:
+                return orig_reconf()
+            ev = {"t": sim.now, "alive": sorted(sim.alive), "serving": list(sim.serving),
+                  "owner": owner_table(sim.plan, H), "shards": shard_table(sim.plan.ffn),
+                  "plan_mode": sim.plan.mode,
+                  "residents": [req_state(sim, rid) for rid in sim.residents],
+                  "routing": [[rid, sim.routing[rid]] for rid in sim.residents],
+                  "backed": [[rid, sim.backup.backed.get(rid, 0)] for rid in sim.residents]}
+            gen0 = sim.reconf_gen
+            orig_reconf()
+            if sim.reconf_gen == gen0:
+                return
+            payload = [e[3] for e in sim.heap if e[3][0] == "reconfig_done"
+                       and e[3][1] == sim.reconf_gen][0]
+            _, _, desired, new_plan, new_routing, merged = payload
+            ev["desired"] = list(desired)
+            ev["new_owner"] = owner_table(new_plan, H)
+            ev["new_shards"] = shard_table(new_plan.ffn)
+            ev["new_routing"] = sorted([rid, g] for rid, g in new_routing.items())
+            ev["recompute"] = sorted([rid, n] for rid, n in merged.recompute_tokens.items())
+            ev["pcie_bytes"] = merged.total_pcie_bytes()
+            ev["gen"] = sim.reconf_gen
+            events.append(ev)
+
+        def done(payload):
+            preempted.clear()
+            orig_done(payload)
+            if payload[1] != sim.reconf_gen or not events or events[-1]["gen"] != payload[1]:
+                return
+            ev = events[-1]
+            ev["after"] = {
+                "serving": list(sim.serving),
+                "routing": sorted([rid, g] for rid, g in sim.routing.items()),
+                "residents": list(sim.residents), "waiting": list(sim.waiting),
+                "preempted": list(preempted),
+                "capacity": sorted([g, v] for g, v in sim.capacity.items()),
+                "reserved": sorted([g, v] for g, v in sim.reserved.items()),
+                "workload": sorted([g, v] for g, v in sim.sched.workload.items()),
+                "waiting_state": [req_state(sim, rid) for rid in sim.waiting]}
+
+        def preempt(rid):
+            preempted.append(rid)
+            orig_preempt(rid)
+
+        sim._reconfigure, sim._handle_reconfig_done, sim._preempt = reconf, done, preempt
+        try:
+            sim.run()
+            stopped = None
+        except KeyError as exc:
+            stopped = f"KeyError {exc} at t={sim.now}"
+        scenarios.append({"name": name, "hbm_bytes_per_gpu": hbm, "failures": csv,
+                          "switch_latency": 0.5, "events": events, "reference_stopped": stopped})
+    return {"scenarios": scenarios, "model": "llama70b.toml",
+            "trace": "mooncake_small.csv[:40]"}
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     gens = (("placement", gen_placement), ("routing", gen_routing),
             ("recovery", gen_recovery), ("forward", gen_forward), ("decode", gen_decode),
             ("batches", gen_batches), ("prefill", gen_prefill), ("metrics", gen_metrics),
-            ("costmodel", gen_costmodel))
+            ("costmodel", gen_costmodel), ("reconfig", gen_reconfig))
     only = sys.argv[1:]
     for name, fn in gens:
         if only and name not in only:

@@ -117,6 +117,78 @@ def _decode_requests(batch: int, ctx: int, out_len: int):
                        tokens_prefilled=ctx - 1, tokens_decoded=1) for i in range(batch)}
 
 
+class WeightStaging:
+    """K7 staging of one GPU for a weight plan (recovery.py:348-427): the
+    head-layers it receives (on-demand: every lost head-layer, at the same
+    offsets on every survivor, so peers can pull each other's slices) and
+    the FFN shards it receives, in the canonical piece layout
+    (hostmirror.WeightLayout).  ``pcie(store_ptr)`` lists the plan's
+    ``pcie_host`` transfers to this GPU (host store -> staging),
+    ``nvlink(peer_bases)`` its ``nvlink_peer`` remainders (peer staging ->
+    staging; the peers loaded those slices from host first)."""
+
+    def __init__(self, wplan, me: int, survivors, layout, num_layers: int):
+        self.plan, self.me, self.layout, self.L = wplan, me, layout, num_layers
+        self.survivors = list(survivors)
+        self.slices = _split_bytes(layout.head_bytes, len(self.survivors))
+        self.starts = np.concatenate([[0], np.cumsum(self.slices)]).astype(np.int64).tolist()
+        mine = [t for t in wplan.transfers if t.dest_gpu == me]
+        self.heads = sorted({tuple(t.detail[:2]) for t in mine if t.content == "attn_head_slice"})
+        self.shards = sorted({t.detail[0] for t in mine if t.content == "ffn_shard"})
+        self.nbytes = len(self.heads) * layout.head_bytes + \
+            len(self.shards) * num_layers * layout.shard_bytes
+
+    def bind(self, base: int) -> dict:
+        """Staging at device address ``base``; returns the pieces map
+        HybridDecodeRank.adopt consumes."""
+        lay = self.layout
+        self.base = base
+        self.head_at = {hl: base + k * lay.head_bytes for k, hl in enumerate(self.heads)}
+        sb = base + len(self.heads) * lay.head_bytes
+        self.shard_at = {(layer, s): sb + (k * self.L + layer) * lay.shard_bytes
+                         for k, s in enumerate(self.shards) for layer in range(self.L)}
+        pieces = {("head", l_, h_): a for (l_, h_), a in self.head_at.items()}
+        pieces.update({("shard", l_, s_): a for (l_, s_), a in self.shard_at.items()})
+        return pieces
+
+    def pcie(self, store_ptr: int) -> SegmentCopy:
+        lay, seg = self.layout, SegmentCopy()
+        for t in self.plan.transfers:
+            if t.dest_gpu != self.me or t.medium != "pcie_host":
+                continue
+            if t.content == "ffn_shard":
+                s = t.detail[0]
+                for layer in range(self.L):
+                    seg.add_bytes(self.shard_at[(layer, s)], store_ptr + lay.shard_off(layer, s),
+                                  lay.shard_bytes)
+            elif len(t.detail) == 3:  # on-demand: this GPU's slice i
+                layer, h, i = t.detail
+                a = self.starts[i]
+                seg.add_bytes(self.head_at[(layer, h)] + a, store_ptr + lay.head_off(layer, h) + a,
+                              self.slices[i])
+            else:                     # fresh reload: the whole head-layer
+                layer, h = t.detail
+                seg.add_bytes(self.head_at[(layer, h)], store_ptr + lay.head_off(layer, h),
+                              lay.head_bytes)
+        return seg
+
+    def nvlink(self, peer_bases: dict) -> SegmentCopy:
+        """peer_bases: survivor index j -> that survivor's staging base (as
+        mapped here); the other survivors' slices of every head-layer."""
+        seg = SegmentCopy()
+        if not any(t.medium == "nvlink_peer" and t.dest_gpu == self.me
+                   for t in self.plan.transfers):
+            return seg
+        i_me = self.survivors.index(self.me)
+        for j, b in peer_bases.items():
+            if j == i_me:
+                continue
+            for hl, a in self.head_at.items():
+                off = (a - self.base) + self.starts[j]
+                seg.add_bytes(self.base + off, b + off, self.slices[j])
+        return seg
+
+
 class ClusterRank:
     """Rank ``rank`` of a hybrid-attention decode world over ``alive``.
 
@@ -280,39 +352,16 @@ class ClusterRank:
         t = lap("plan", t_event)
 
         # 2. K7: staging = every lost head-layer (same offsets on every
-        #    survivor) + this GPU's lost shards
-        lay = self.layout
-        i_me = survivors.index(me)
-        slices = _split_bytes(lay.head_bytes, len(survivors))
-        starts = np.concatenate([[0], np.cumsum(slices)]).tolist()
-        heads = sorted({t_.detail[:2] for t_ in wplan.transfers if t_.content == "attn_head_slice"})
-        my_shards = sorted(t_.detail[0] for t_ in wplan.transfers
-                           if t_.content == "ffn_shard" and t_.dest_gpu == me)
-        n_bytes = len(heads) * lay.head_bytes + len(my_shards) * model.num_layers * lay.shard_bytes
-        # cudaMalloc'd (not the caching allocator): IPC exports whole allocations
+        #    survivor) + this GPU's lost shards; cudaMalloc'd (not the
+        #    caching allocator): IPC exports whole allocations
+        stg = WeightStaging(wplan, me, survivors, self.layout, model.num_layers)
         sp = C.c_void_p()
         dev_index = self.device.index if self.device.index is not None \
             else torch.cuda.current_device()
-        N.check(N.lib.fs_ar_alloc(dev_index, max(n_bytes, 256), C.byref(sp)), "fs_ar_alloc")
+        N.check(N.lib.fs_ar_alloc(dev_index, max(stg.nbytes, 256), C.byref(sp)), "fs_ar_alloc")
         base = sp.value
-        head_at = {hl: base + k * lay.head_bytes for k, hl in enumerate(heads)}
-        shard_base = base + len(heads) * lay.head_bytes
-        shard_at = {(layer, s): shard_base + (k * model.num_layers + layer) * lay.shard_bytes
-                    for k, s in enumerate(my_shards) for layer in range(model.num_layers)}
-        h2d = SegmentCopy()
-        w = self.wstore.dev_ptr
-        for t_ in wplan.transfers:
-            if t_.dest_gpu != me or t_.medium != "pcie_host":
-                continue
-            if t_.content == "ffn_shard":
-                s = t_.detail[0]
-                for layer in range(model.num_layers):
-                    h2d.add_bytes(shard_at[(layer, s)], w + lay.shard_off(layer, s),
-                                  lay.shard_bytes)
-            else:
-                layer, h, i = t_.detail
-                a = starts[i]
-                h2d.add_bytes(head_at[(layer, h)] + a, w + lay.head_off(layer, h) + a, slices[i])
+        pieces = stg.bind(base)
+        h2d = stg.pcie(self.wstore.dev_ptr)
         h2d.run(self.device)
         rep.weight_pcie_bytes = h2d.bytes
         t = lap("weights_pcie", t)
@@ -320,9 +369,8 @@ class ClusterRank:
         handle = (C.c_uint8 * 64)()
         N.check(N.lib.fs_ar_ipc_handle(C.c_void_p(base), handle), "fs_ar_ipc_handle")
         every = self.ctl.all_gather_object(bytes(handle))
-        p2p = SegmentCopy()
-        opened = []
-        if heads:
+        opened, peer_bases = [], {}
+        if stg.heads:
             for j, g in enumerate(survivors):
                 if g == me:
                     continue
@@ -330,9 +378,8 @@ class ClusterRank:
                 N.check(N.lib.fs_ar_ipc_open((C.c_uint8 * 64).from_buffer_copy(every[j]),
                                              C.byref(q)), "fs_ar_ipc_open")
                 opened.append(q.value)
-                for k, hl in enumerate(heads):
-                    off = k * lay.head_bytes + starts[j]
-                    p2p.add_bytes(base + off, q.value + off, slices[j])
+                peer_bases[j] = q.value
+        p2p = stg.nvlink(peer_bases)
         p2p.run(self.device)
         rep.weight_nvlink_bytes = p2p.bytes
         t = lap("weights_nvlink", t)
@@ -344,8 +391,6 @@ class ClusterRank:
         # 3. in-place adoption
         new_owner = owner_array(new_plan, model.num_kv_heads)
         new_shards = [new_plan.ffn.owner[s] for s in range(new_plan.ffn.num_shards)]
-        pieces = {("head", l_, h_): a for (l_, h_), a in head_at.items()}
-        pieces.update({("shard", l_, s_): a for (l_, s_), a in shard_at.items()})
         fresh = eng.adopt(new_owner, new_routing, new_shards, pieces)
         eng.set_lengths([self.ctx] * self.batch)
         N.lib.fs_ar_free(C.c_void_p(base))

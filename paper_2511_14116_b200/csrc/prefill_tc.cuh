@@ -428,6 +428,10 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1) prefill_tc_kernel(const Pref
         for (int j = 0; j < nb; ++j) {
             const int b = j % kSBuf, hb = 2 * h + b;
             mbar_wait(s_full + 8 * hb, (j / kSBuf) & 1);
+            // consume o_done of block j - kSBuf: S_j was issued after that
+            // block's P.V, so it has retired (returns at once) -- every
+            // o_done phase is observed (the epilogue takes the last ones)
+            if (j >= kSBuf) mbar_wait(o_done + 8 * hb, ((j - kSBuf) / kSBuf) & 1);
             tc_after();
             constexpr int kC = kTcKeys / 32;  // 32-column groups of S
             uint32_t sr[kC][32];

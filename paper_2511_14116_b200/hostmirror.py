@@ -224,6 +224,19 @@ class WeightStore:
             self.region.unlink()
 
 
+class HostWeightStore:
+    """Single-process weight store (pinned host memory, same layout and
+    interface as :class:`WeightStore`) for the one-process emulation."""
+
+    def __init__(self, layout: WeightLayout):
+        self.layout = layout
+        self.host = torch.empty(layout.total, dtype=torch.uint8, pin_memory=True)
+        self.dev_ptr = self.host.data_ptr()  # pinned + UVA: device-addressable
+
+    def close(self, unlink: bool = False) -> None:
+        self.host = None
+
+
 # --------------------------------------------------------------- copies --
 _SEG = np.dtype([("src", np.uint64), ("dst", np.uint64), ("spitch", np.int64),
                  ("dpitch", np.int64), ("width", np.int64), ("height", np.int64)])

@@ -398,6 +398,22 @@ class HybridDecodeRank:
         seg.run(self.device)
         return seg.bytes
 
+    def load_pieces(self, pieces) -> int:
+        """Overwrite every slot's and shard's weights from canonical pieces
+        (``adopt``'s ``pieces`` map): a GPU reloading its whole assignment
+        (expansion, recovery.py:366-394).  One launch; returns bytes."""
+        from .hostmirror import SegmentCopy
+        seg = SegmentCopy()
+        for layer in range(self.model.num_layers):
+            for j, h in enumerate(self.work.slot_heads[layer]):
+                self._from_piece(seg, self._head_parts(layer, j), pieces[("head", layer, h)])
+            if self.mlp:
+                for k, sh in enumerate(self.shards):
+                    self._from_piece(seg, self._shard_parts(layer, k), pieces[("shard", layer, sh)])
+        seg.run(self.device)
+        torch.cuda.current_stream(self.device).synchronize()
+        return seg.bytes
+
     def adopt(self, owner, routing, shard_owner, pieces) -> np.ndarray:
         """Adopt a new placement IN PLACE (the on-demand shrink target,
         recovery.py:396-427, after re-routing): KV pages of every (layer,
@@ -413,6 +429,14 @@ class HybridDecodeRank:
             raise ValidationError("adopt needs the cuBLAS weight layout")
         old_work = self.work
         work = RankWork.build(np.asarray(owner, dtype=np.int32), self.rank, routing, self.batch)
+        new_shards = sorted(s_ for s_, g in enumerate(shard_owner) if g == self.rank) \
+            if self.mlp else self.shards
+        if work.slot_heads == old_work.slot_heads and new_shards == self.shards:
+            # same slots and shards (a routing change): only the KV tables move
+            fresh = self.cache.adopt(work)
+            self.work = work
+            self._graph = None
+            return fresh
         L, hd, hid, qpk = self.model.num_layers, self.model.head_dim, self.model.hidden_dim, self.qpk
         S = work.n_slots
         rw = S * (qpk + 2) * hd

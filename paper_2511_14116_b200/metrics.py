@@ -132,6 +132,7 @@ class RunRecorder:
         self.buckets = {}
         self.prefill_tokens = self.decode_tokens = self.recomputed = 0
         self.completed = 0
+        self.preempted = 0
         self.done = set()
 
     def iteration(self, batch, duration_s: float, per_rank_s=None, finished_prefill=()):
@@ -187,6 +188,15 @@ class RunRecorder:
     def failure(self, gpu: int, alive: int):
         self.log.add("failure", t=round(self.now, 9), gpu=gpu, alive=alive)
 
+    def recovery(self, gpu: int, alive: int):
+        """A GPU rejoined (simulation.py:626-633)."""
+        self.log.add("recovery", t=round(self.now, 9), gpu=gpu, alive=alive)
+
+    def preemption(self, rid: int):
+        """A resident preempted over KV capacity (simulation.py:283-310)."""
+        self.preempted += 1
+        self.log.add("preemption", t=round(self.now, 9), request=rid)
+
     def reconfig(self, world: int, recovery_s: float, recomputed_tokens: int, pcie_bytes: int):
         """A measured reconfiguration: the world stalls for ``recovery_s``."""
         self.log.add("reconfig_start", t=round(self.now, 9), world=world,
@@ -205,7 +215,8 @@ class RunRecorder:
         iters = [r["compute_ratio"] for r in self.log.of_kind("iteration")
                  if r["compute_ratio"] is not None]
         self.log.add(
-            "run_summary", t=round(end, 9), completed=self.completed, rejected=0, preempted=0,
+            "run_summary", t=round(end, 9), completed=self.completed, rejected=0,
+            preempted=self.preempted,
             prefill_tokens=self.prefill_tokens, decode_tokens=self.decode_tokens,
             recomputed_tokens=self.recomputed,
             prefill_throughput=round(self.prefill_tokens / end, 6) if end > 0 else 0.0,

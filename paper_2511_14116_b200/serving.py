@@ -228,7 +228,8 @@ class HybridServingRank(HybridDecodeRank):
 
     def __init__(self, model, owner, rank: int, routing, request_capacity, max_tokens: int,
                  device=None, seed: int = 0, group=None, mlp: bool = True, shard_owner=None,
-                 config: int = 0, page_order: str = "contiguous", exchange: str = "nccl"):
+                 config: int = 0, page_order: str = "contiguous", exchange: str = "nccl",
+                 reserve_pages: int = 0):
         cap = np.asarray(request_capacity, dtype=np.int64)
         if cap.ndim != 1 or cap.size == 0 or cap.min() < 1:
             raise ValidationError("request_capacity must list >= 1 token per request")
@@ -236,9 +237,17 @@ class HybridServingRank(HybridDecodeRank):
                          device=device, seed=seed, group=group, page_order=page_order,
                          config=config, mlp=mlp, shard_owner=shard_owner,
                          request_capacity=cap, exchange=exchange,
-                         exchange_elems=int(max_tokens) * model.hidden_dim)
+                         exchange_elems=int(max_tokens) * model.hidden_dim,
+                         reserve_pages=reserve_pages)
         self.request_capacity = cap
         self.max_tokens = int(max_tokens)
+        self._derive()
+
+    def _derive(self) -> None:
+        """Buffers and tables that follow the work / slot layout (rebuilt
+        after an in-place adoption)."""
+        model = self.model
+        cap = self.request_capacity
         S, hd, qpk, hid = self.n_slots, model.head_dim, self.qpk, model.hidden_dim
         self.row_width = S * (qpk + 2) * hd
         dev = self.device
@@ -271,6 +280,12 @@ class HybridServingRank(HybridDecodeRank):
         # per iteration, the fully served (TP) slots are not
         self.partial_slots = [np.nonzero((self.item_index_all[l] < 0).any(axis=1))[0].tolist()
                               for l in range(model.num_layers)]
+
+    def adopt(self, owner, routing, shard_owner, pieces) -> np.ndarray:
+        """In-place adoption (HybridDecodeRank.adopt) + the serving tables."""
+        fresh = super().adopt(owner, routing, shard_owner, pieces)
+        self._derive()
+        return fresh
 
     def plan(self, batch: StepBatch) -> StepPlan:
         return StepPlan(self, batch)

@@ -4,7 +4,7 @@
 # Usage (on the GPU box): bash tools/sanitize.sh
 set -u
 OUT=gpurun_out/sanitize
-mkdir -p $OUT
+rm -rf $OUT; mkdir -p $OUT
 CS="compute-sanitizer --print-limit 50 --target-processes all"
 SMOKE="python -c 'import __graft_entry__ as g; g.smoke()'"
 TESTS=(
@@ -14,6 +14,8 @@ TESTS=(
   "tests/test_exchange_gpu.py::test_fused_exchange_ordered_sum"
   "tests/test_recovery_gpu.py::test_backup_then_restore_is_bitexact"
   "tests/test_recovery_gpu.py::test_restore_failed_rank_onto_survivor_per_plan"
+  "tests/test_gemm_gpu.py::test_store"
+  "tests/test_exchange_gpu.py::test_fused_exchange_decode_step_matches_emulation"
 )
 for tool in memcheck racecheck synccheck; do
   echo "== $tool smoke" | tee -a $OUT/summary.txt
