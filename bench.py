@@ -547,26 +547,42 @@ def cost_calibration(fstates, mixed, batch=64, ctx=4096, fails=(7, 3, 5), budget
         groups["mixed"].append((PlanCost(plan, model, ref, cluster), work,
                                 {r["rank"]: r["iter_ms"][i] / 1e3 for r in mixed["ranks"]}))
 
-    def rms_err(params, samples):
-        errs = []
-        for pc, work, meas in samples:
-            pc2 = PlanCost(pc.plan, model, params, cluster)
-            pred = pc2.per_gpu_compute_time(work)
-            errs += [pred[g] / t - 1.0 for g, t in meas.items()]
-        return float(np.sqrt(np.mean(np.square(errs))))
+    from paper_2511_14116_b200.costmodel import calibrate_b200, rms_error
 
-    import numpy as np
-    out = {"model": "reference costmodel.py (per-layer straggler max, linear in tokens / "
-                    "context tokens / token-shards), fitted per regime by NNLS on relative "
-                    "error; gpu_throughput = 1 (constants in seconds)"}
-    for name, samples in list(groups.items()) + [("both", groups["decode"] + groups["mixed"])]:
-        fit, err = calibrate(samples)
-        out[name] = {"attn_s_per_head_token": fit.attn_flop_per_head_token,
-                     "attn_s_per_head_ctx_token": fit.attn_flop_per_head_ctx_token,
-                     "ffn_s_per_token_shard": fit.ffn_flop_per_token_per_shard,
-                     "rms_rel_err": round(err, 4),
-                     "reference_flop_model_rms_rel_err": round(rms_err(ref, samples), 4),
-                     "samples": sum(len(m) for _, _, m in samples)}
+    def ref_form(params):
+        return lambda pc, work: PlanCost(pc.plan, model, params, cluster).per_gpu_compute_time(work)
+
+    dec = groups["decode"]
+    train_dec = [s_ for s_, st in zip(dec, fstates["states"]) if st["world"] >= 7]
+    test_dec = [s_ for s_, st in zip(dec, fstates["states"]) if st["world"] < 7]
+    out = {"model": "reference costmodel.py features (attention per head-token and per "
+                    "head-context-token, FFN per token-shard; per-GPU compute time), fitted by "
+                    "NNLS on relative error (gpu_throughput = 1, constants in seconds); "
+                    "'b200' adds the two terms a B200 decode step has and the FLOP model lacks: "
+                    "seconds per resident weight byte and a fixed per-iteration cost",
+           "reference_flop_constants_rms_rel_err": {
+               "decode": round(rms_error(ref_form(ref), dec), 4),
+               "mixed": round(rms_error(ref_form(ref), groups["mixed"]), 4)}}
+    for name, train, test in (("decode_8_7_predicts_6_5", train_dec, test_dec),
+                              ("decode_predicts_mixed_c5", dec, groups["mixed"]),
+                              ("joint_in_sample", dec + groups["mixed"], [])):
+        fit3, err3 = calibrate(train)
+        fit5, err5 = calibrate_b200(train)
+        out[name] = {
+            "reference_form": {"attn_s_per_head_token": fit3.attn_flop_per_head_token,
+                               "attn_s_per_head_ctx_token": fit3.attn_flop_per_head_ctx_token,
+                               "ffn_s_per_token_shard": fit3.ffn_flop_per_token_per_shard,
+                               "train_rms_rel_err": round(err3, 4),
+                               "heldout_rms_rel_err": round(rms_error(ref_form(fit3), test), 4)
+                               if test else None},
+            "b200": {"coef": [float(c) for c in fit5.coef],
+                     "terms": ["attn_s_per_head_token", "attn_s_per_head_ctx_token",
+                               "ffn_s_per_token_shard", "s_per_weight_byte", "fixed_s"],
+                     "train_rms_rel_err": round(err5, 4),
+                     "heldout_rms_rel_err": round(rms_error(fit5.per_gpu_time, test), 4)
+                     if test else None},
+            "train_samples": sum(len(m) for _, _, m in train),
+            "test_samples": sum(len(m) for _, _, m in test)}
     return out
 
 

@@ -85,3 +85,30 @@ def test_calibration_recovers_constants():
     assert fit.attn_flop_per_head_token == pytest.approx(2e-9, rel=1e-5)
     assert fit.attn_flop_per_head_ctx_token == pytest.approx(3e-12, rel=1e-5)
     assert fit.ffn_flop_per_token_per_shard == pytest.approx(5e-9, rel=1e-5)
+
+
+def test_b200_calibration_recovers_weight_and_fixed_terms():
+    """The extended model (reference features + weight bytes + fixed) is
+    recovered from synthetic measurements and predicts HELD-OUT worlds."""
+    from paper_2511_14116_b200.costmodel import CalibratedCost, calibrate_b200, rms_error
+    model, cluster = _llama70b()
+    true = CalibratedCost([2e-9, 3e-12, 5e-9, 1.6e-13, 4e-4])
+    ref = CostParams.from_model(model)
+    rng = np.random.default_rng(1)
+
+    def samples(worlds):
+        out = []
+        for world, fail in worlds:
+            pc = PlanCost(_plan(model, "hybrid", world, fail), model, ref, cluster)
+            for _ in range(3):
+                ranks = pc.ranks
+                work = _work([["decode", r, ranks[r % len(ranks)], int(rng.integers(100, 8000))]
+                              for r in range(64)] +
+                             [["prefill", 64 + i, ranks[i % len(ranks)], 0,
+                               int(rng.integers(1, 500))] for i in range(3)])
+                out.append((pc, work, true.per_gpu_time(pc, work)))
+        return out
+    train, test = samples([(8, None), (8, 7)]), samples([(6, None), (5, None)])
+    fit, err = calibrate_b200(train)
+    assert err < 1e-6
+    assert rms_error(fit.per_gpu_time, test) < 1e-6
