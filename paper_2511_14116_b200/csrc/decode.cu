@@ -523,6 +523,8 @@ static int launch_decode(const DecodeParams &prm, int sms, cudaStream_t st) {
     auto fn = KIND == 0 ? decode_kernel<WARPS, STAGES, CTAS> : decode_cta_kernel<WARPS, STAGES>;
     if (!attr_set[dev & 63]) {
         FS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     (int)cudaSharedmemCarveoutMaxShared));
         attr_set[dev & 63] = true;
     }
     // PDL: with FS_DECODE_EARLY_PREFETCH the prologue (table lookups, first

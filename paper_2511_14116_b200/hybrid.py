@@ -265,6 +265,21 @@ class HybridDecodeRank:
         for layer in range(self.model.num_layers):
             g(x, self.p_qkv[layer], self.qkv, STORE)
             self.cache.decode_layer_fused(layer, self.qkv, self.o)
+            if self.xchg is not None and self.group is not None:
+                # partials straight into the symmetric exchange buffers;
+                # fs_ar_residual does the ordered sum + residual
+                ia, im = (0, 1) if self.mlp else (layer & 1, None)
+                g(o2, self.p_o[layer], self.xchg.partial(ia, x.shape), STORE)
+                self.xchg.reduce_residual(ia, x)
+                if self.mlp:
+                    part = self.xchg.partial(im, x.shape)
+                    if len(self.ffn_cols):
+                        g(x, self.p_gu[layer], self.act, SWIGLU)
+                        g(self.act, self.p_d[layer], part, STORE)
+                    else:
+                        part.zero_()
+                    self.xchg.reduce_residual(im, x)
+                continue
             if self.group is None:
                 g(o2, self.p_o[layer], x, RESIDUAL)
             else:
@@ -506,8 +521,9 @@ class HybridDecodeRank:
         split-tile reduction launch (gemm="tcgen05")."""
         has_mlp = self.mlp and len(self.ffn_cols)
         if self.gemm == "tcgen05":
-            return self.model.num_layers * (1 + 2 * (4 if has_mlp else 2))
-        n = self.model.num_layers * (2 if has_mlp else 1)
+            n = self.model.num_layers * (1 + 2 * (4 if has_mlp else 2))
+        else:
+            n = self.model.num_layers * (2 if has_mlp else 1)
         if self.xchg is not None:  # one fs_ar_residual per exchange
             n += self.model.num_layers * (2 if self.mlp else 1)
         if self.backup_ptr is not None:  # token backup
