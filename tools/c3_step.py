@@ -14,20 +14,27 @@ ap.add_argument("--rank", type=int, default=0)
 ap.add_argument("--gemm", default="cublas")
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--time", action="store_true", help="graph-time the step instead")
+ap.add_argument("--pf", default="", help="L2 prefetch mode (HybridDecodeRank.set_l2_prefetch)")
+ap.add_argument("--pf-ctas", type=int, default=16)
+ap.add_argument("--model", default="70b")
 a = ap.parse_args()
-model = bench.llama70b()
-plan = make_placement("hybrid", model, range(8))
-alive = list(range(8))
-for f in (7, 3, 5)[:8 - a.world]:
+model = bench.llama70b() if a.model == "70b" else bench.llama8b()
+base = 8 if a.model == "70b" else a.world
+plan = make_placement("hybrid", model, range(base))
+alive = list(range(base))
+for f in (7, 3, 5)[:base - a.world]:
     alive = [g for g in alive if g != f]
     plan = plan_weight_recovery(model, plan, alive, "on_demand").target_plan("hybrid", model)
 routing = bench.route(64, alive, 4096)
 bench.GEMM_BACKEND = a.gemm
 eng = bench.build_rank(model, plan, a.rank, routing, 64, 4096, None, 0)
+if a.pf:
+    eng.set_l2_prefetch(a.pf, a.pf_ctas)
+    eng.capture()
 if a.time:
     ms = bench.time_graph(eng.step, 10, 3)
     wb, kb = eng.weight_bytes(), bench.step_kv_bytes(eng)
-    print(f"world {a.world} rank {a.rank} {a.gemm}: step {ms:.3f} ms, weights {wb/1e9:.2f} GB "
+    print(f"{a.model} world {a.world} rank {a.rank} {a.gemm} pf={a.pf or '-'}/{a.pf_ctas}: step {ms:.3f} ms, weights {wb/1e9:.2f} GB "
           f"kv {kb/1e9:.2f} GB, {(wb+kb)/ms/1e6:.0f} GB/s")
 else:
     for _ in range(a.steps):
