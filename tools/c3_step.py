@@ -14,8 +14,6 @@ ap.add_argument("--rank", type=int, default=0)
 ap.add_argument("--gemm", default="cublas")
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--time", action="store_true", help="graph-time the step instead")
-ap.add_argument("--pf", default="", help="L2 prefetch mode (HybridDecodeRank.set_l2_prefetch)")
-ap.add_argument("--pf-ctas", type=int, default=16)
 ap.add_argument("--model", default="70b")
 a = ap.parse_args()
 model = bench.llama70b() if a.model == "70b" else bench.llama8b()
@@ -28,13 +26,10 @@ for f in (7, 3, 5)[:base - a.world]:
 routing = bench.route(64, alive, 4096)
 bench.GEMM_BACKEND = a.gemm
 eng = bench.build_rank(model, plan, a.rank, routing, 64, 4096, None, 0)
-if a.pf:
-    eng.set_l2_prefetch(a.pf, a.pf_ctas)
-    eng.capture()
 if a.time:
     ms = bench.time_graph(eng.step, 10, 3)
     wb, kb = eng.weight_bytes(), bench.step_kv_bytes(eng)
-    print(f"{a.model} world {a.world} rank {a.rank} {a.gemm} pf={a.pf or '-'}/{a.pf_ctas}: step {ms:.3f} ms, weights {wb/1e9:.2f} GB "
+    print(f"{a.model} world {a.world} rank {a.rank} {a.gemm}: step {ms:.3f} ms, weights {wb/1e9:.2f} GB "
           f"kv {kb/1e9:.2f} GB, {(wb+kb)/ms/1e6:.0f} GB/s")
 else:
     for _ in range(a.steps):
