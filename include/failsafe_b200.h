@@ -351,15 +351,21 @@ int fs_fill_normal(void *out, int64_t rows, int64_t cols, int64_t ld,
 
 /* ---- the exchange: ordered-sum all-reduce + residual over peer memory ----
  * (refexec.py:283-307).  Each rank owns symmetric buffers of
- * fs_ar_buffer_bytes(max_elems) bytes (fs_ar_alloc: zeroed cudaMalloc),
- * shares them with CUDA IPC (fs_ar_ipc_handle -> 64-byte handle ->
- * fs_ar_ipc_open on every peer) and writes its bf16 partial to the first
- * n elements of its own buffer.  fs_ar_residual then signals / waits on the
- * peers' flags and does x[i] += bf16(sum over ranks 0..world-1, in order,
- * in fp32, of partial_r[i]) in ONE launch (peers[r] = buffer of rank r as
- * mapped in this process, data_bytes = the buffer's flag offset =
+ * fs_ar_buffer_bytes(max_elems) bytes (fs_ar_alloc: zeroed cudaMalloc;
+ * layout [partial][slice sums][flags]), shares them with CUDA IPC
+ * (fs_ar_ipc_handle -> 64-byte handle -> fs_ar_ipc_open on every peer) and
+ * writes its bf16 partial to the first n elements of its own buffer.
+ * fs_ar_residual then signals / waits on the peers' flags and does
+ * x[i] += bf16(sum over ranks 0..world-1, in order, in fp32, of
+ * partial_r[i]) in ONE launch (peers[r] = buffer of rank r as mapped in
+ * this process, data_bytes = the buffer's flag offset =
  * fs_ar_buffer_bytes(max_elems) - 256).  Consecutive exchanges must
- * alternate between two buffers.  Traps (no hang) if a peer never arrives. */
+ * alternate between two buffers.  Traps (no hang) if a peer never arrives.
+ * fs_ar_residual_mode: mode 1 = one-shot (every rank reads every partial),
+ * 2 = two-shot (each rank sums its 1/world slice, then gathers the rounded
+ * slices: (world-1)/world of the vector read twice instead of world-1
+ * times), 0 = auto (two-shot for world > 2 and >= 256 KiB); identical
+ * bits in every mode.  fs_ar_residual = mode 0. */
 #define FS_AR_MAX_WORLD 16
 int64_t fs_ar_buffer_bytes(int64_t max_elems);
 int fs_ar_alloc(int device, int64_t bytes, void **ptr);
@@ -369,6 +375,8 @@ int fs_ar_ipc_open(const void *handle64, void **ptr);
 int fs_ar_ipc_close(void *ptr);
 int fs_ar_residual(void *const *peers, int32_t rank, int32_t world, int64_t n,
                    int64_t data_bytes, void *x, int32_t ctas, void *stream);
+int fs_ar_residual_mode(void *const *peers, int32_t rank, int32_t world, int64_t n,
+                        int64_t data_bytes, void *x, int32_t ctas, int32_t mode, void *stream);
 
 /* K7: enable peer access (idempotent) and peer copy */
 int fs_enable_peer(int device, int peer);

@@ -121,6 +121,8 @@ _SIGS = {
     "fs_ar_ipc_close": (C.c_int, [C.c_void_p]),
     "fs_ar_residual": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int64,
                                  C.c_int64, C.c_void_p, C.c_int32, C.c_void_p]),
+    "fs_ar_residual_mode": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int64,
+                                      C.c_int64, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     "fs_enable_peer": (C.c_int, [C.c_int, C.c_int]),
     "fs_copy_peer": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int64,
                                C.c_void_p]),

@@ -9,7 +9,10 @@ signals the peers, waits for them, and does ``x += bf16(sum_r partial_r)``
 reading the partials in rank order -- the reference's exact ordered sum,
 bit-identical on every rank, with no NCCL launch and no separate residual
 add.  Two buffers alternate between consecutive exchanges (the kernel's
-flag protocol needs no second barrier then).
+flag protocol needs no second barrier then).  Large vectors on more than two
+ranks use the kernel's two-shot form (each rank sums its 1/N slice, then
+gathers the rounded slices), which reads 2(N-1)/N instead of N-1 vectors
+over NVLink per rank and gives the same bits.
 """
 
 from __future__ import annotations
@@ -50,6 +53,7 @@ class FusedExchange:
         if self.world > N.FS_AR_MAX_WORLD:
             raise ValidationError(f"fused exchange supports up to {N.FS_AR_MAX_WORLD} ranks")
         self.max_elems = int(max_elems) + (-int(max_elems)) % 8
+        self.mode = 0  # fs_ar_residual_mode: automatic one-shot / two-shot
         self.nbytes = int(N.lib.fs_ar_buffer_bytes(self.max_elems))
         self.data_bytes = self.nbytes - 256
         self._own, self._opened = [], []
@@ -125,27 +129,29 @@ class FusedExchange:
             raise ValidationError("partial larger than the exchange buffer")
         return self._views[i][:n].view(*shape)
 
-    def reduce_residual(self, i: int, x: torch.Tensor) -> None:
+    def reduce_residual(self, i: int, x: torch.Tensor, mode: int = None) -> None:
         """``x += bf16(sum over ranks, in rank order, of partial_r)`` where
-        partial_r is rank r's buffer ``i`` (its first ``x.numel()`` elements)."""
+        partial_r is rank r's buffer ``i`` (its first ``x.numel()`` elements).
+        ``mode``: 1 one-shot, 2 two-shot, 0 / None automatic (``self.mode``)."""
         if x.dtype != torch.bfloat16 or not x.is_contiguous() or x.numel() % 8:
             raise ValidationError("x must be contiguous bf16 with a multiple of 8 elements")
         st = torch.cuda.current_stream(self.device).cuda_stream
-        N.check(N.lib.fs_ar_residual(self.peers[i], self.rank, self.world, x.numel(),
-                                     self.data_bytes, C.c_void_p(x.data_ptr()), 0,
-                                     C.c_void_p(st)), "fs_ar_residual")
+        N.check(N.lib.fs_ar_residual_mode(self.peers[i], self.rank, self.world, x.numel(),
+                                          self.data_bytes, C.c_void_p(x.data_ptr()), 0,
+                                          self.mode if mode is None else mode,
+                                          C.c_void_p(st)), "fs_ar_residual")
 
     def _self_check(self) -> None:
-        """One exchange on each buffer with rank-keyed data, checked against
-        the ordered sum every rank can recompute."""
+        """Exchanges on each buffer, one-shot and two-shot, with rank-keyed
+        data, checked against the ordered sum every rank can recompute."""
         n = min(self.max_elems, 4096)
-        for i in range(2):
+        for i, mode in ((0, 1), (1, 1), (0, 2), (1, 2)):
             parts = [torch.randn(n, generator=torch.Generator().manual_seed(1000 * r + i))
                      .to(torch.bfloat16) for r in range(self.world)]
             self.partial(i, (n,)).copy_(parts[self.rank].to(self.device))
             x = torch.ones(n, dtype=torch.bfloat16, device=self.device)
             torch.cuda.current_stream(self.device).synchronize()
-            self.reduce_residual(i, x)
+            self.reduce_residual(i, x, mode)
             total = torch.zeros(n)
             for p in parts:
                 total += p.float()

@@ -34,12 +34,12 @@ def _init(rank, world, port):
     return dist
 
 
-def _exchange_worker(rank, world, port, q):
+def _exchange_worker(rank, world, port, q, mode=0, n=64 * 512):
     try:
         dist = _init(rank, world, port)
         from paper_2511_14116_b200.collective import FusedExchange
-        n = 64 * 512
         xc = FusedExchange(dist.group.WORLD, n, "cuda:0")
+        xc.mode = mode
         x = torch.randn(n, generator=torch.Generator().manual_seed(7)).to(torch.bfloat16)
         want = x.clone()
         xd = x.cuda()
@@ -85,7 +85,19 @@ def test_fused_exchange_ordered_sum(world):
         assert ok and same, (rank, ok, same)
 
 
-def _step_worker(rank, world, port, q):
+@pytest.mark.parametrize("world,mode,n", [(2, 2, 64 * 512), (3, 2, 64 * 512), (3, 1, 64 * 8192),
+                                          (3, 2, 64 * 8192), (3, 2, 8 * 1001), (4, 2, 8)])
+def test_fused_exchange_two_shot(world, mode, n):
+    """The two-shot form (slice sums, then gather) gives the one-shot's exact
+    ordered sums, also for slices of unequal length and fewer elements than
+    ranks' slices (n = 8: three empty slices)."""
+    res = _run(_exchange_worker, world, mode, n)
+    for rank, ok, same, err in res:
+        assert err is None, err
+        assert ok and same, (rank, ok, same)
+
+
+def _step_worker(rank, world, port, q, gemm="cublas"):
     try:
         dist = _init(rank, world, port)
         from paper_2511_14116_b200.core import ModelSpec
@@ -101,7 +113,7 @@ def _step_worker(rank, world, port, q):
 
         def engine(g, group, exchange):
             e = HybridDecodeRank(model, owner, g, routing, len(lens), 64, seed=3, group=group,
-                                 mlp=True, shard_owner=shards, exchange=exchange)
+                                 mlp=True, shard_owner=shards, exchange=exchange, gemm=gemm)
             e.set_lengths(lens)
             e.fill_random_kv(11 + g)
             return e
@@ -126,8 +138,13 @@ def _step_worker(rank, world, port, q):
         q.put((rank, False, False, repr(e)))
 
 
-def test_fused_exchange_decode_step_matches_emulation():
-    for rank, ok, ok2, err in _run(_step_worker, 2):
+@pytest.mark.parametrize("gemm", ["cublas", "tcgen05"])
+def test_fused_exchange_decode_step_matches_emulation(gemm):
+    """Eager and graph-captured 2-rank steps with the fused exchange equal
+    the single-process emulation bit for bit, with the cuBLAS projections
+    and with the tcgen05 skinny GEMM writing straight into the exchange
+    buffers."""
+    for rank, ok, ok2, err in _run(_step_worker, 2, gemm):
         assert err is None, err
         assert ok and ok2, (rank, ok, ok2)
 

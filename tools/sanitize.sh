@@ -16,6 +16,7 @@ TESTS=(
   "tests/test_recovery_gpu.py::test_restore_failed_rank_onto_survivor_per_plan"
   "tests/test_gemm_gpu.py::test_store"
   "tests/test_exchange_gpu.py::test_fused_exchange_decode_step_matches_emulation"
+  "tests/test_exchange_gpu.py::test_fused_exchange_two_shot"
 )
 for tool in memcheck racecheck synccheck; do
   echo "== $tool smoke" | tee -a $OUT/summary.txt
