@@ -49,7 +49,7 @@ METRIC = ("decode tokens/s at 8→7→6→5 B200 (fraction of HBM roofline); "
           "failure recovery ms")
 UNIT = "tokens/s"
 KV_UNIT = 512  # bytes per (kv head, token): K+V, head_dim 128, bf16 (core.py:101-103)
-GEMM_BACKEND = "cublas"  # --gemm: projections via cuBLAS or the tcgen05 skinny GEMM
+GEMM_BACKEND = "tcgen05"  # --gemm: projections via the tcgen05 skinny GEMM (default) or cuBLAS
 EXCHANGE = "fused"
 # fs_decode_attention configs -> the kernel instance that runs (csrc/decode.cu)
 KERNEL_NAMES = {0: "decode_cta_kernel<8,2>", 3: "decode_cta_kernel<16,1>",
@@ -796,7 +796,7 @@ def main():
     ap.add_argument("--skip-mixed", action="store_true",
                     help="skip the config-5 mixed prefill/decode trace section")
     ap.add_argument("--skip-cpu", action="store_true")
-    ap.add_argument("--gemm", default="cublas", choices=("cublas", "tcgen05"))
+    ap.add_argument("--gemm", default="tcgen05", choices=("tcgen05", "cublas"))
     ap.add_argument("--exchange", default="fused", choices=("fused", "nccl"),
                     help="N>1 exchange: one fs_ar_residual kernel over IPC-mapped peer "
                          "buffers (default) or an NCCL all-reduce + add")

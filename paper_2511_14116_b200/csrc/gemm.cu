@@ -2,28 +2,38 @@
 //     out[n, c] (+)= sum_k x[n, k] * W[k, c]        n < 64 (the decode batch)
 // computed as D^T[128 cols x 64 rows] = W^T-tile . x^T with tcgen05.mma
 // (M = 128 weight columns, N = 64 batch rows, K = 16 per instruction; A = the
-// W tile, MN-major, B = x, K-major, both TMA-loaded with 128B swizzle; the
-// fp32 accumulator lives in TMEM, double-buffered).
+// W tile, MN-major, B = x, K-major 128B-swizzled; fp32 accumulators in TMEM).
 //
-// Work decomposition is stream-K over (column tile, 64-wide k-step) units:
-// the persistent grid (one CTA per SM) splits the U = tiles x K/64 units
-// evenly, so skinny shapes with few column tiles (Llama-70B qkv at 8 GPUs:
-// 10 tiles) still use every SM and every byte of W is read exactly once.  A
-// CTA that covers a whole tile applies the epilogue directly; otherwise it
-// writes an fp32 partial to slot `tile + cta`, and gemm_reduce_kernel (the
-// next launch, PDL) sums each split tile's partials in CTA order
-// (deterministic) and applies the epilogue.
+// Work decomposition: data-parallel split-K.  A CTA owns one column GROUP
+// (G = 1 or 2 adjacent 128-column tiles) and one of S equal k-ranges of it;
+// grid = groups x S <= the SM count, so every byte of W is read once and
+// (almost) every SM streams.  Why not stream-K: one SM's TMA stream is
+// bounded by bulk copies per second, not bytes (tools/ubench/stream_probe:
+// 8 KB copies cap at ~58 GB/s per SM, 32 KB copies reach ~200 GB/s, and
+// >= 96 SMs streaming 16-32 KB copies saturate HBM), so a CTA streams ONE
+// contiguous W region in 32 KB bulk copies (weights pre-packed in the UMMA
+// K-major SWIZZLE_128B layout, a group's k-range contiguous) and x in 16 KB
+// tensor copies; stream-K's split tiles also cost a reduction launch.
+//
+// The S splits of a group are one thread-block cluster.  Each CTA puts its
+// fp32 partial tile in its own shared memory; after a cluster barrier every
+// CTA sums its 1/S slice of the rows over all S tiles through distributed
+// shared memory, in split order (deterministic), and applies the epilogue;
+// a second barrier keeps the tiles alive for their readers.  No workspace,
+// no semaphores, no reduction launch.  S <= 8 is the largest split count
+// whose clusters are all co-resident (cudaOccupancyMaxActiveClusters).
 //
 // Roles (192 threads): warp 4 = TMA producer, warp 5 = MMA issuer, warps 0-3
 // = epilogue (TMEM lane quadrant = warp index).  Fused epilogues: plain
 // store, residual add (x += ...), and SwiGLU (tile = 64 gate + 64 up
 // columns -> 64 activations).  Launched with programmatic dependent launch:
-// W tiles of the first stages are fetched before griddepcontrol.wait, so the
-// weight stream starts while the previous kernel drains.
+// the first W stages are fetched before griddepcontrol.wait, so the weight
+// stream starts while the previous kernel drains.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <mutex>
 #include <unordered_map>
 
@@ -31,24 +41,30 @@
 
 namespace fs {
 
-constexpr int kGemmStages = 8;
+constexpr int kGemmStages = 4;
 constexpr int kTileM = 128;        // weight columns per tile (UMMA M)
 constexpr int kRowsN = 64;         // batch rows (UMMA N)
-constexpr int kStepK = 64;         // k per stage (one 128B swizzle row)
-constexpr int kStageA = kTileM * kStepK * 2;   // 16 KB (two 64-col boxes)
-constexpr int kStageB = kRowsN * kStepK * 2;   // 8 KB
-constexpr int kStageBytes = kStageA + kStageB;
-constexpr int kUpPitch = 64 + 4;              // fp32 row pitch of the swiglu 'up' stage
+constexpr int kStepK = 64;         // k per step (one 128B swizzle row of x)
+constexpr int kBlockW = kTileM * kStepK * 2;   // 16 KB: one (tile, step) W block
+constexpr int kBlockX = kRowsN * kStepK * 2;   // 8 KB: one step of x
+constexpr int kStageW = 2 * kBlockW;           // 32 KB: 2 steps x 1 tile or 1 step x 2 tiles
+constexpr int kStageX = 2 * kBlockX;           // 16 KB
+constexpr int kStageBytes = kStageW + kStageX;
 constexpr int kGemmThreads = 192;
 constexpr int kPrefetchA = 3;   // W stages issued before the PDL wait
+constexpr int kMaxGroup = 2;
+constexpr int kMaxSplits = 8;                 // portable cluster size
+constexpr int kOtPitch = kMaxGroup * kTileM + 4;  // fp32 output-tile row pitch
+
 
 enum GemmEpilogue { EPI_STORE = 0, EPI_RESIDUAL = 1, EPI_SWIGLU = 2 };
 
 struct GemmParams {
     int32_t rows;       // valid batch rows (<= 64)
-    int32_t K;          // multiple of 64
+    int32_t nk;         // K / 64
     int32_t tiles;      // output column tiles of 128
-    int64_t n_units;    // tiles * K/64
+    int32_t group;      // G: tiles per CTA (1 or 2)
+    int32_t splits;     // k-ranges per group
     int32_t epilogue;
     int32_t w_packed;   // 1: W pre-packed in UMMA-canonical 16 KB blocks
     const uint8_t *w_raw;
@@ -56,8 +72,8 @@ struct GemmParams {
     int64_t ld_out;
     const __nv_bfloat16 *res;
     int64_t ld_res;
-    float *ws;          // partial slots, each [64][128] fp32
-    int32_t *sems;      // reserved (ABI): split tiles are reduced by gemm_reduce_kernel
+    float *ws;          // partial slots, each [64][128] fp32, slot = cta * G + g
+    int32_t *sems;      // per group: arrive, depart (self-resetting)
     unsigned long long *dbg;  // optional per-CTA phase timestamps (ns)
 };
 
@@ -135,12 +151,15 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
 // kind::f16 instruction descriptor: BF16 x BF16 -> F32, A MN-major, B K-major
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) |
                             ((uint32_t)(kRowsN >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
+constexpr uint32_t kIdescK = kIdesc & ~(1u << 15);   // A K-major
 
-__device__ __forceinline__ int64_t gemm_owner(int64_t u, int64_t C, int64_t U) {
-    return ((u + 1) * C + U - 1) / U - 1;
-}
-__device__ __forceinline__ bool gemm_live(int64_t c, int64_t C, int64_t U) {
-    return c * U / C < (c + 1) * U / C;
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, int c0, int c1,
+                                            int c2, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -149,49 +168,109 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-__device__ __forceinline__ int ld_acquire(const int32_t *p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ float silu(float g) { return g / (1.f + __expf(-g)); }
+
+// Output writer shared by both paths: rows [0, nr) of the CTA's output
+// region (global rows row0 + r) in 16-byte chunks, consecutive threads on
+// consecutive chunks (coalesced), residual loads of a round issued before
+// any use.  val(r, col, v) fills v[8] with the fp32 GEMM values of CTA-local
+// columns col..col+7 (col in [0, 128 G)).  STORE / RESIDUAL: chunk = 8
+// output columns; SWIGLU: chunk = 8 activations from gate col and up col+64.
+template <int G, typename Val>
+__device__ __forceinline__ void gemm_write(const GemmParams &p, int grp, int row0, int nr,
+                                           int t, Val val) {
+    const bool swiglu = p.epilogue == EPI_SWIGLU, resid = p.epilogue == EPI_RESIDUAL;
+    const int cpr = (swiglu ? 8 : 16) * G;  // chunks per row
+    const int total = nr * cpr;
+    constexpr int U = 4;
+    for (int base = 0; base < total; base += U * 128) {
+        // every load of the round first (residual rows, values), then use
+        uint4 rv[U];
+        float v[U][8], w[U][8];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int idx = base + u * 128 + t;
+            rv[u] = make_uint4(0, 0, 0, 0);
+            if (idx < total) {
+                const int r = idx / cpr, ch = idx % cpr;
+                if (swiglu) {
+                    const int g = ch >> 3, a = (ch & 7) * 8;
+                    val(r, g * kTileM + a, v[u]);
+                    val(r, g * kTileM + 64 + a, w[u]);
+                } else {
+                    val(r, ch * 8, v[u]);
+                    if (resid)
+                        rv[u] = *reinterpret_cast<const uint4 *>(
+                            p.res + (int64_t)(row0 + r) * p.ld_res + (int64_t)(grp * G) * kTileM + ch * 8);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int idx = base + u * 128 + t;
+            if (idx >= total) break;
+            const int r = idx / cpr, ch = idx % cpr;
+            uint4 o;
+            if (swiglu) {
+                const int g = ch >> 3, a = (ch & 7) * 8;
+                o.x = pack_bf16(silu(v[u][0]) * w[u][0], silu(v[u][1]) * w[u][1]);
+                o.y = pack_bf16(silu(v[u][2]) * w[u][2], silu(v[u][3]) * w[u][3]);
+                o.z = pack_bf16(silu(v[u][4]) * w[u][4], silu(v[u][5]) * w[u][5]);
+                o.w = pack_bf16(silu(v[u][6]) * w[u][6], silu(v[u][7]) * w[u][7]);
+                *reinterpret_cast<uint4 *>(p.out + (int64_t)(row0 + r) * p.ld_out +
+                                           (int64_t)(grp * G + g) * 64 + a) = o;
+            } else {
+                if (resid) {
+                    const uint32_t q[4] = {rv[u].x, rv[u].y, rv[u].z, rv[u].w};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        v[u][2 * i] += __uint_as_float(q[i] << 16);
+                        v[u][2 * i + 1] += __uint_as_float(q[i] & 0xffff0000u);
+                    }
+                }
+                o.x = pack_bf16(v[u][0], v[u][1]);
+                o.y = pack_bf16(v[u][2], v[u][3]);
+                o.z = pack_bf16(v[u][4], v[u][5]);
+                o.w = pack_bf16(v[u][6], v[u][7]);
+                *reinterpret_cast<uint4 *>(p.out + (int64_t)(row0 + r) * p.ld_out +
+                                           (int64_t)(grp * G) * kTileM + ch * 8) = o;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+                 "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+
+// (no memory clobber: the tiles are read-only between the two cluster
+// barriers, so the loads of a round may be batched)
+__device__ __forceinline__ float4 ld_dsmem_v4(uint32_t addr) {
+    float4 v;
+    asm("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+        : "r"(addr));
     return v;
 }
 
-__device__ __forceinline__ float silu(float g) { return g / (1.f + __expf(-g)); }
-
-// final epilogue straight from the accumulator registers: thread m owns
-// column m of the tile for all 64 rows, so for a fixed row a warp stores 32
-// consecutive bf16.  SwiGLU: warps 2-3 (the 'up' columns) stage through
-// shared memory, warps 0-1 (gate) combine and store the 64 activations.
-__device__ __forceinline__ void gemm_epilogue(const GemmParams &p, const float (&acc)[kRowsN],
-                                              int tile, int m, float *up) {
-    if (p.epilogue == EPI_SWIGLU) {
-        if (m >= 64) {
-#pragma unroll
-            for (int n = 0; n < kRowsN; ++n) up[n * kUpPitch + (m - 64)] = acc[n];
-        }
-        named_bar_sync(2, 128);
-        if (m < 64) {
-#pragma unroll
-            for (int n = 0; n < kRowsN; ++n)
-                if (n < p.rows)
-                    p.out[n * p.ld_out + tile * 64 + m] =
-                        __float2bfloat16_rn(silu(acc[n]) * up[n * kUpPitch + m]);
-        }
-        return;
-    }
-    const int64_t col = (int64_t)tile * kTileM + m;
-    if (p.epilogue == EPI_RESIDUAL) {
-#pragma unroll
-        for (int n = 0; n < kRowsN; ++n)
-            if (n < p.rows)
-                p.out[n * p.ld_out + col] =
-                    __float2bfloat16_rn(acc[n] + __bfloat162float(p.res[n * p.ld_res + col]));
-    } else {
-#pragma unroll
-        for (int n = 0; n < kRowsN; ++n)
-            if (n < p.rows) p.out[n * p.ld_out + col] = __float2bfloat16_rn(acc[n]);
-    }
+// one lane of the (converged) warp: true on exactly one lane
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+                 : "=r"(pred));
+    return pred != 0;
 }
 
+// A (W^T tile) K-major when the weights are packed (KMAJ), MN-major when
+// they are TMA-loaded from the row-major [K][N] matrix
+template <int G, bool KMAJ>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_skinny_kernel(const __grid_constant__ CUtensorMap map_w,
                        const __grid_constant__ CUtensorMap map_x, const GemmParams p) {
@@ -200,20 +279,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint8_t *smem = reinterpret_cast<uint8_t *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = smem_u32(smem);
-    float *up = reinterpret_cast<float *>(smem + kGemmStages * kStageBytes);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kGemmStages * kStageBytes +
-                                                  kRowsN * kUpPitch * 4);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kGemmStages * kStageBytes);
     const uint32_t bar_full = smem_u32(bars);
     const uint32_t bar_empty = bar_full + 8 * kGemmStages;
-    const uint32_t bar_acc_full = bar_empty + 8 * kGemmStages;   // [2]
-    const uint32_t bar_acc_empty = bar_acc_full + 16;            // [2]
+    const uint32_t bar_acc = bar_empty + 8 * kGemmStages;
     __shared__ uint32_t s_tmem;
 
-
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t C = gridDim.x, U = p.n_units, c = blockIdx.x;
-    const int64_t u0 = c * U / C, u1 = (c + 1) * U / C;
-    const int nk = p.K / kStepK;
+    const int S = p.splits;
+    const int grp = blockIdx.x / S, split = blockIdx.x % S;
+    const int k0 = (int)((int64_t)split * p.nk / S), k1 = (int)((int64_t)(split + 1) * p.nk / S);
+    constexpr int sps = G == 1 ? 2 : 1;                // k-steps per stage
+    const int n_st = (k1 - k0 + sps - 1) / sps;        // >= 1 (splits <= nk)
+    constexpr uint32_t tcols = G == 1 ? 64u : 128u;
 
     if (warp == 4 && lane == 0) {
         prefetch_tmap(&map_w);
@@ -222,226 +300,185 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             mbar_init(bar_full + 8 * s, 1);
             mbar_init(bar_empty + 8 * s, 1);
         }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(bar_acc_full + 8 * b, 1);
-            mbar_init(bar_acc_empty + 8 * b, 128);
-        }
+        mbar_init(bar_acc, 1);
         fence_barrier_init();
         fence_proxy_async();
     }
-    if (warp == 0) {  // TMEM: two 64-column fp32 accumulators
+    if (warp == 0) {  // TMEM: G 64-column fp32 accumulators
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(&s_tmem)),
-                     "r"(128));
+                     "r"(tcols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = s_tmem;
-    if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 8 + 0] = gtimer();
+    if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 16 + 0] = gtimer();
 
-    if (u0 < u1) {
-        if (warp == 4) {
-            // ---------------- TMA producer ----------------
-            if (lane == 0) {
-                const uint64_t pol = policy_evict_first();
-                int stage = 0;
-                uint32_t phase = 0;
-                int issued = 0;
-                bool waited = false;
-                int t = (int)(u0 / nk), ks = (int)(u0 % nk);  // advanced incrementally
-                for (int64_t u = u0; u < u1; ++u, ks = (ks + 1 == nk) ? (++t, 0) : ks + 1) {
-                    mbar_wait(bar_empty + 8 * stage, phase ^ 1u);
-                    const uint32_t a = sbase + stage * kStageBytes, b = a + kStageA;
-                    mbar_expect_tx(bar_full + 8 * stage, kStageBytes);
-                    if (p.w_packed) {  // one contiguous 16 KB block, one bulk copy
-                        bulk_g2s(a, p.w_raw + ((int64_t)t * nk + ks) * kStageA, kStageA,
-                                 bar_full + 8 * stage, pol);
-                    } else {
-                        tma_load_2d(a, &map_w, t * kTileM, ks * kStepK, bar_full + 8 * stage);
-                        tma_load_2d(a + kStageA / 2, &map_w, t * kTileM + 64, ks * kStepK,
-                                    bar_full + 8 * stage);
-                    }
-                    if (!waited && (++issued == kPrefetchA || u + 1 == u1)) {
-                        // x comes from the preceding kernel: PDL wait, then
-                        // the B halves of every stage issued so far
-                        if (p.dbg) p.dbg[blockIdx.x * 8 + 5] = gtimer();
-                        grid_dependency_wait();
-                        waited = true;
-                        if (p.dbg) p.dbg[blockIdx.x * 8 + 6] = gtimer();
-                        int st = stage, vks = ks;
-                        for (int i = 0; i < issued; ++i) {
-                            tma_load_2d(sbase + st * kStageBytes + kStageA, &map_x, vks * kStepK,
-                                        0, bar_full + 8 * st);
-                            st = st == 0 ? kGemmStages - 1 : st - 1;
-                            vks = vks == 0 ? nk - 1 : vks - 1;
-                        }
-                    } else if (waited) {
-                        tma_load_2d(b, &map_x, ks * kStepK, 0, bar_full + 8 * stage);
-                    }
-                    if (++stage == kGemmStages) {
-                        stage = 0;
-                        phase ^= 1u;
-                    }
-                }
-                asm volatile("griddepcontrol.launch_dependents;");
-            }
-        } else if (warp == 5) {
-            // ---------------- MMA issuer ----------------
-            if (lane == 0) {
-                int stage = 0;
-                uint32_t phase = 0;
-                int seg = 0;
-                int64_t u = u0;
-                while (u < u1) {
-                    const int t = (int)(u / nk);
-                    const int64_t seg_end = min(u1, (int64_t)(t + 1) * nk);
-                    const int buf = seg & 1;
-                    mbar_wait(bar_acc_empty + 8 * buf, ((seg >> 1) & 1) ^ 1u);
-                    tc_fence_after();
-                    const uint32_t d = tmem + buf * kRowsN;
-                    bool first = true;
-                    for (; u < seg_end; ++u) {
-                        mbar_wait(bar_full + 8 * stage, phase);
-                        if (p.dbg && u == u0) p.dbg[blockIdx.x * 8 + 1] = gtimer();
-                        tc_fence_after();
-                        const uint32_t a = sbase + stage * kStageBytes, b = a + kStageA;
-#pragma unroll
-                        for (int j = 0; j < kStepK / 16; ++j) {
-                            // packed: no-swizzle canonical MN-major (k-group
-                            // stride 2048 B = LBO, m-group stride 128 B = SBO)
-                            const uint64_t ad = p.w_packed
-                                                    ? umma_desc(a + j * 4096, 2048, 128, 0)
-                                                    : umma_desc(a + j * 2048, kStageA / 2, 1024, 2);
-                            const uint64_t bd = umma_desc(b + j * 32, 16, 1024, 2);
-                            tc_mma(d, ad, bd, kIdesc, first ? 0u : 1u);
-                            first = false;
-                        }
-                        tc_commit(bar_empty + 8 * stage);
-                        if (++stage == kGemmStages) {
-                            stage = 0;
-                            phase ^= 1u;
-                        }
-                    }
-                    tc_commit(bar_acc_full + 8 * buf);
-                    if (p.dbg) p.dbg[blockIdx.x * 8 + 2] = gtimer();
-                    ++seg;
-                }
-            }
-        } else {
-            // ---------------- epilogue (warps 0-3) ----------------
-            const int m = warp * 32 + lane;
-            int seg = 0;
-            int64_t u = u0;
-            while (u < u1) {
-                const int t = (int)(u / nk);
-                const int64_t tb = (int64_t)t * nk, te = tb + nk;
-                const int64_t seg_end = min(u1, te);
-                const bool whole = u == tb && seg_end == te;
-                const int buf = seg & 1;
-                mbar_wait(bar_acc_full + 8 * buf, (seg >> 1) & 1);
-                tc_fence_after();
-                float acc[kRowsN];
-                {
-                    float v[32];
-                    const uint32_t taddr = tmem + buf * kRowsN + ((uint32_t)(warp * 32) << 16);
-                    tmem_ld32(taddr, v);
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) acc[i] = v[i];
-                    tmem_ld32(taddr + 32, v);
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) acc[32 + i] = v[i];
-                }
-                tc_fence_before();
-                mbar_arrive(bar_acc_empty + 8 * buf);
-                if (whole) {
-                    gemm_epilogue(p, acc, t, m, up);
-                    named_bar_sync(2, 128);  // 'up' staging reused by the next segment
+    if (warp == 4) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            int stage = 0;
+            uint32_t phase = 0;
+            bool waited = false;
+            auto issue_x = [&](int st, int s_idx) {
+                tma_load_3d(sbase + s_idx * kStageBytes + kStageW, &map_x, 0, 0, k0 + st * sps,
+                            bar_full + 8 * s_idx);
+            };
+            for (int st = 0; st < n_st; ++st) {
+                mbar_wait(bar_empty + 8 * stage, phase ^ 1u);
+                const int a = k0 + st * sps, n = min(sps, k1 - a);
+                const uint32_t ws_ = sbase + stage * kStageBytes;
+                mbar_expect_tx(bar_full + 8 * stage, n * G * kBlockW + sps * kBlockX);
+                if (p.w_packed) {  // one contiguous region: blocks [group][step][g]
+                    bulk_g2s(ws_, p.w_raw + ((int64_t)grp * p.nk + a) * G * kBlockW,
+                             n * G * kBlockW, bar_full + 8 * stage, pol);
                 } else {
-                    // split tile: this CTA's fp32 partial goes to slot
-                    // tile + cta; gemm_reduce_kernel (the next launch, PDL)
-                    // sums a tile's partials in CTA order -- no CTA of this
-                    // grid ever waits for another
-                    const int64_t slot = (int64_t)t + c;
-                    float *wsl = p.ws + slot * (kRowsN * kTileM);
-#pragma unroll
-                    for (int n = 0; n < kRowsN; ++n) __stcg(wsl + n * kTileM + m, acc[n]);
+                    for (int i = 0; i < n; ++i) {
+                        tma_load_2d(ws_ + i * kBlockW, &map_w, grp * kTileM, (a + i) * kStepK,
+                                    bar_full + 8 * stage);
+                        tma_load_2d(ws_ + i * kBlockW + kBlockW / 2, &map_w, grp * kTileM + 64,
+                                    (a + i) * kStepK, bar_full + 8 * stage);
+                    }
                 }
-                if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 8 + 3] = gtimer();
-                u = seg_end;
-                ++seg;
+                if (!waited && (st + 1 == kPrefetchA || st + 1 == n_st)) {
+                    // x comes from the preceding kernel: PDL wait, then the
+                    // x halves of every stage issued so far
+                    if (p.dbg) p.dbg[blockIdx.x * 16 + 5] = gtimer();
+                    grid_dependency_wait();
+                    waited = true;
+                    if (p.dbg) p.dbg[blockIdx.x * 16 + 6] = gtimer();
+                    for (int i = 0; i <= st; ++i) issue_x(i, i);  // st < kGemmStages
+                } else if (waited) {
+                    issue_x(st, stage);
+                }
+                if (++stage == kGemmStages) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
             }
-            if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 8 + 3] = gtimer();
+            grid_launch_dependents();
+        }
+    } else if (warp == 5) {
+        // ---------------- MMA issuer ----------------
+        // The whole warp runs the loop, so descriptors and TMEM addresses are
+        // warp-uniform (uniform datapath); one elected lane issues.  W and x
+        // stages are both SWIZZLE_128B, x K-major; W K-major when packed
+        // (128 column rows of 128 B, 8-row groups 1 KB apart = SBO), else
+        // MN-major (two 64-column halves 8 KB apart = LBO, 8-row k groups
+        // 1 KB apart = SBO).
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int st = 0; st < n_st; ++st) {
+            mbar_wait(bar_full + 8 * stage, phase);
+            if (p.dbg && st == 0 && lane == 0) p.dbg[blockIdx.x * 16 + 1] = gtimer();
+            tc_fence_after();
+            const int n = min(sps, k1 - (k0 + st * sps));
+            const uint32_t a = sbase + stage * kStageBytes, b = a + kStageW;
+            if (elect_one()) {
+#pragma unroll
+                for (int i = 0; i < sps; ++i) {
+                    if (i < n) {
+#pragma unroll
+                        for (int g = 0; g < G; ++g) {
+                            const uint32_t ab = a + (i * G + g) * kBlockW;
+#pragma unroll
+                            for (int j = 0; j < kStepK / 16; ++j) {
+                                const uint64_t ad = KMAJ ? umma_desc(ab + j * 32, 16, 1024, 2)
+                                                         : umma_desc(ab + j * 2048, kBlockW / 2, 1024, 2);
+                                const uint64_t bd = umma_desc(b + i * kBlockX + j * 32, 16, 1024, 2);
+                                tc_mma(tmem + g * kRowsN, ad, bd, KMAJ ? kIdescK : kIdesc,
+                                       (st | i | j) ? 1u : 0u);
+                            }
+                        }
+                    }
+                }
+                tc_commit(bar_empty + 8 * stage);
+            }
+            __syncwarp();
+            if (++stage == kGemmStages) {
+                stage = 0;
+                phase ^= 1u;
+            }
+        }
+        if (elect_one()) tc_commit(bar_acc);
+        __syncwarp();
+        if (p.dbg && lane == 0) p.dbg[blockIdx.x * 16 + 2] = gtimer();
+    } else {
+        // ---------------- epilogue (warps 0-3) ----------------
+        // accumulators -> fp32 tile [64][128 G + 4] over the (drained) stage
+        // ring: thread m owns column m (TMEM lane) for all 64 rows
+        const int m = warp * 32 + lane;
+        mbar_wait(bar_acc, 0);
+        tc_fence_after();
+        grid_dependency_wait();  // out / res: after the previous kernel
+        if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 16 + 8] = gtimer();
+        float *ot = reinterpret_cast<float *>(smem);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                float v[32];
+                tmem_ld32(tmem + g * kRowsN + h * 32 + ((uint32_t)(warp * 32) << 16), v);
+#pragma unroll
+                for (int n = 0; n < 32; ++n) ot[(h * 32 + n) * kOtPitch + g * kTileM + m] = v[n];
+            }
+        }
+        if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 16 + 3] = gtimer();
+        if (S == 1) {
+            named_bar_sync(1, 128);
+            gemm_write<G>(p, grp, 0, p.rows, m, [&](int r, int col, float (&v)[8]) {
+                const float4 *q = reinterpret_cast<const float4 *>(ot + r * kOtPitch + col);
+                const float4 x0 = q[0], x1 = q[1];
+                v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
+                v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+            });
         }
     }
-    if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 8 + 4] = gtimer();
+    if (S > 1) {
+        // ---- split reduction over distributed shared memory: the group's
+        // splits are one thread-block cluster (rank = split).  Each CTA sums
+        // its 1/S slice of the rows over every split's tile, in split order
+        // (deterministic), and writes it; a second cluster barrier keeps
+        // every tile alive until its readers are done ----
+        __syncwarp();
+        cluster_sync_all();  // all S partial tiles are in shared memory
+        if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 16 + 7] = gtimer();
+        if (warp < 4) {
+            const int r0 = split * p.rows / S, r1 = (split + 1) * p.rows / S;
+            gemm_write<G>(p, grp, r0, r1 - r0, threadIdx.x, [&](int r, int col, float (&v)[8]) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] = 0.f;
+                const uint32_t off = sbase + (uint32_t)(((r0 + r) * kOtPitch + col) * 4);
+                for (int sb = 0; sb < S; sb += 4) {  // 4 splits' loads in flight
+                    float4 x[4][2];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        if (sb + i < S) {
+                            const uint32_t q = mapa_shared(off, (uint32_t)(sb + i));
+                            x[i][0] = ld_dsmem_v4(q);
+                            x[i][1] = ld_dsmem_v4(q + 16);
+                        }
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)  // split order: deterministic
+                        if (sb + i < S) {
+                            v[0] += x[i][0].x; v[1] += x[i][0].y; v[2] += x[i][0].z; v[3] += x[i][0].w;
+                            v[4] += x[i][1].x; v[5] += x[i][1].y; v[6] += x[i][1].z; v[7] += x[i][1].w;
+                        }
+                }
+            });
+        }
+        if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 16 + 10] = gtimer();
+        cluster_sync_all();  // peers are done reading this CTA's tile
+    }
+    if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 16 + 4] = gtimer();
     tc_fence_before();
     __syncthreads();
     if (warp == 0) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
-    }
-}
-
-// Split tiles of a stream-K launch: block (tile, 8-row group); thread m sums
-// column m of the tile over the contributors' partials in CTA order
-// (deterministic) and applies the epilogue.  Blocks of whole tiles exit.
-// Launched with PDL right behind gemm_skinny_kernel: scheduled during its
-// tail, waits in griddepcontrol.wait for its partials.
-constexpr int kRedRows = 8;
-
-__global__ void __launch_bounds__(kTileM) gemm_reduce_kernel(const GemmParams p, int32_t grid) {
-    const int t = blockIdx.x, r0 = blockIdx.y * kRedRows, m = threadIdx.x;
-    const int nk = p.K / kStepK;
-    const int64_t C = grid, U = p.n_units;
-    const int64_t tb = (int64_t)t * nk, te = tb + nk;
-    const int64_t clo = gemm_owner(tb, C, U), chi = gemm_owner(te - 1, C, U);
-    grid_launch_dependents();
-    if (clo == chi || r0 >= p.rows) return;  // whole tile: the GEMM stored it
-    const bool swiglu = p.epilogue == EPI_SWIGLU;
-    if (swiglu && m >= 64) return;
-    grid_dependency_wait();
-    float g[kRedRows], uu[kRedRows];
-#pragma unroll
-    for (int r = 0; r < kRedRows; ++r) g[r] = uu[r] = 0.f;
-    // 4 contributors' rows in flight per round (a split tile of a small GEMM
-    // has up to ~15 contributors; one round trip per contributor was the
-    // whole cost), summed in CTA order
-    const bool all_live = U >= C;
-    for (int64_t s0 = clo; s0 <= chi; s0 += 4) {
-        float vg[4][kRedRows], vu[4][kRedRows];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int64_t s = s0 + i;
-            const bool ok = s <= chi && (all_live || gemm_live(s, C, U));
-            const float *src = p.ws + (t + (ok ? s : clo)) * (kRowsN * kTileM) + r0 * kTileM + m;
-#pragma unroll
-            for (int r = 0; r < kRedRows; ++r) {
-                vg[i][r] = ok ? __ldcg(src + r * kTileM) : 0.f;
-                vu[i][r] = ok && swiglu ? __ldcg(src + r * kTileM + 64) : 0.f;
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int r = 0; r < kRedRows; ++r) {
-                g[r] += vg[i][r];
-                uu[r] += vu[i][r];
-            }
-    }
-#pragma unroll
-    for (int r = 0; r < kRedRows; ++r) {
-        const int n = r0 + r;
-        if (n >= p.rows) break;
-        if (swiglu) {
-            p.out[n * p.ld_out + t * 64 + m] = __float2bfloat16_rn(silu(g[r]) * uu[r]);
-        } else {
-            const int64_t col = (int64_t)t * kTileM + m;
-            float v = g[r];
-            if (p.epilogue == EPI_RESIDUAL) v += __bfloat162float(p.res[n * p.ld_res + col]);
-            p.out[n * p.ld_out + col] = __float2bfloat16_rn(v);
-        }
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
     }
 }
 
@@ -465,16 +502,14 @@ static EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// 2-D bf16 row-major [rows][cols] (row stride ld elements), box 64 x box_rows
-static int make_map(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
-                    int box_rows) {
+// bf16 tensor map, 128B swizzle; dims / strides innermost first (strides
+// of dims 1.. in bytes)
+static int make_map(CUtensorMap *map, const void *ptr, int rank, const cuuint64_t *dims,
+                    const cuuint64_t *strides, const cuuint32_t *box) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return fail(FS_ECUDA, "cuTensorMapEncodeTiled unavailable");
-    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims,
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void *>(ptr), dims,
                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(FS_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -484,27 +519,67 @@ static int make_map(CUtensorMap *map, const void *ptr, int64_t rows, int64_t col
 static unsigned long long *g_gemm_dbg = nullptr;  // fs_gemm_debug_timestamps
 
 static size_t gemm_smem() {
-    return 1024 + (size_t)kGemmStages * kStageBytes + (size_t)kRowsN * kUpPitch * 4 + 8 * 40;
+    return 1024 + (size_t)kGemmStages * kStageBytes + 8 * 16;
+}
+
+template <int G, bool KMAJ>
+static int max_active_clusters(int device, int S) {
+    // cached per (device, kernel, cluster size)
+    static std::mutex mu;
+    static std::unordered_map<int, int> cache;
+    const int key = device * 64 + S;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(S * 16);
+    lc.blockDim = dim3(kGemmThreads);
+    lc.dynamicSmemBytes = gemm_smem();
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = S;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, gemm_skinny_kernel<G, KMAJ>, &lc) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+    }
+    cache[key] = n;
+    return n;
+}
+
+// the launch plan: k-splits per column group = cluster size, the largest
+// S <= 8 with groups x S <= SMs whose clusters are all co-resident
+template <int G, bool KMAJ>
+static int gemm_splits(int device, int sms, int groups, int nk) {
+    if (groups >= sms) return 1;
+    int s = std::min(std::min(sms / groups, kMaxSplits), nk);
+    for (; s > 1; --s)
+        if (groups <= max_active_clusters<G, KMAJ>(device, s)) break;
+    return std::max(s, 1);
 }
 
 }  // namespace fs
 
 using namespace fs;
 
-// testing hook (not in the public header): per-CTA phase timestamps
 extern "C" void fs_gemm_debug_timestamps(unsigned long long *dev_buf) { g_gemm_dbg = dev_buf; }
 
 extern "C" int64_t fs_gemm_workspace_floats(int device, int32_t N, int32_t epilogue) {
     const int sms = sm_count(device);
     if (sms <= 0 || N <= 0) return -1;
-    const int64_t tiles = (int64_t)N / kTileM;
     (void)epilogue;
-    return (tiles + sms) * (int64_t)kRowsN * kTileM;  // sems: 2 * tiles int32
+    // reserved (ABI): split tiles are reduced over distributed shared
+    // memory, no global workspace is used
+    return 1;
 }
 
 extern "C" int fs_gemm_skinny(const void *x, int64_t ld_x, int32_t rows, int32_t K, const void *w,
-                              int64_t ld_w, int32_t w_layout, int32_t N, void *out, int64_t ld_out, const void *res,
-                              int64_t ld_res, int32_t epilogue, float *workspace,
+                              int64_t ld_w, int32_t w_layout, int32_t N, void *out, int64_t ld_out,
+                              const void *res, int64_t ld_res, int32_t epilogue, float *workspace,
                               int64_t ws_floats, int32_t *sems, int32_t device, void *stream) {
     FS_CHECK_ARG(rows >= 1 && rows <= kRowsN, "rows must be in [1, %d], got %d", kRowsN, rows);
     FS_CHECK_ARG(K > 0 && K % kStepK == 0, "K must be a positive multiple of %d", kStepK);
@@ -512,27 +587,60 @@ extern "C" int fs_gemm_skinny(const void *x, int64_t ld_x, int32_t rows, int32_t
     FS_CHECK_ARG(epilogue >= EPI_STORE && epilogue <= EPI_SWIGLU, "unknown epilogue %d", epilogue);
     FS_CHECK_ARG(x && w && out && workspace && sems, "null pointer");
     FS_CHECK_ARG(epilogue != EPI_RESIDUAL || res, "residual epilogue needs res");
-    FS_CHECK_ARG(ld_x % 8 == 0 && ld_w % 8 == 0 && ld_x >= K && (w_layout == 1 || ld_w >= N),
+    FS_CHECK_ARG(w_layout >= 0 && w_layout <= 2, "unknown W layout %d", w_layout);
+    FS_CHECK_ARG(ld_x % 8 == 0 && ld_x >= K && (w_layout != 0 || (ld_w % 8 == 0 && ld_w >= N)),
                  "leading dimensions must be multiples of 8 and cover the matrix");
+    FS_CHECK_ARG(ld_out % 8 == 0 && (epilogue != EPI_RESIDUAL || ld_res % 8 == 0) &&
+                     (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(res) & 15) == 0,
+                 "out / res must be 16-byte aligned with row strides that are multiples of 8");
+    const int group = w_layout == 2 ? 2 : 1;
+    const int tiles = N / kTileM;
+    FS_CHECK_ARG(tiles % group == 0, "W layout 2 needs an even number of 128-column tiles");
     const int sms = sm_count(device);
     if (sms <= 0) return fail(FS_ECUDA, "cannot query SM count");
     FS_CHECK_ARG(ws_floats >= fs_gemm_workspace_floats(device, N, epilogue), "workspace too small");
+    const int nk = K / kStepK;
+    const int sps = group == 1 ? 2 : 1;
     CUtensorMap mw, mx;
-    FS_CHECK_ARG(w_layout == 0 || w_layout == 1, "unknown W layout %d", w_layout);
-    if (int rc = make_map(&mx, x, rows, K, ld_x, kRowsN)) return rc;
-    if (w_layout == 1) {
+    {   // x as [K/64][rows][64]: one copy = sps k-steps of 64 rows, 8 KB each
+        cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)nk};
+        cuuint64_t strides[2] = {(cuuint64_t)ld_x * 2, 128};
+        cuuint32_t box[3] = {64, (cuuint32_t)kRowsN, (cuuint32_t)sps};
+        if (int rc = make_map(&mx, x, 3, dims, strides, box)) return rc;
+    }
+    if (w_layout != 0) {
         FS_CHECK_ARG((reinterpret_cast<uintptr_t>(w) & 15) == 0, "packed W must be 16B aligned");
         mw = mx;  // unused: packed blocks are moved with 1-D bulk copies
     } else {
-        if (int rc = make_map(&mw, w, K, N, ld_w, kStepK)) return rc;
+        cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)K};
+        cuuint64_t strides[1] = {(cuuint64_t)ld_w * 2};
+        cuuint32_t box[2] = {64, (cuuint32_t)kStepK};
+        if (int rc = make_map(&mw, w, 2, dims, strides, box)) return rc;
     }
     GemmParams prm;
     prm.rows = rows;
-    prm.K = K;
-    prm.tiles = N / kTileM;
-    prm.n_units = (int64_t)prm.tiles * (K / kStepK);
+    prm.nk = nk;
+    prm.tiles = tiles;
+    prm.group = group;
+    const size_t smem = gemm_smem();
+    static bool attr_set[64] = {false};
+    if (!attr_set[device & 63]) {
+        FS_CUDA(cudaFuncSetAttribute(gemm_skinny_kernel<1, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FS_CUDA(cudaFuncSetAttribute(gemm_skinny_kernel<1, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FS_CUDA(cudaFuncSetAttribute(gemm_skinny_kernel<2, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set[device & 63] = true;
+    }
+    const int groups = tiles / group;
+    prm.splits = w_layout == 0 ? gemm_splits<1, false>(device, sms, groups, nk)
+                 : group == 1  ? gemm_splits<1, true>(device, sms, groups, nk)
+                               : gemm_splits<2, true>(device, sms, groups, nk);
+    const int grid = groups * prm.splits;
     prm.epilogue = epilogue;
-    prm.w_packed = w_layout;
+    prm.w_packed = w_layout != 0;
     prm.w_raw = static_cast<const uint8_t *>(w);
     prm.dbg = g_gemm_dbg;
     prm.out = static_cast<__nv_bfloat16 *>(out);
@@ -541,31 +649,25 @@ extern "C" int fs_gemm_skinny(const void *x, int64_t ld_x, int32_t rows, int32_t
     prm.ld_res = ld_res;
     prm.ws = workspace;
     prm.sems = sems;
-    const size_t smem = gemm_smem();
-    static bool attr_set[64] = {false};
-    if (!attr_set[device & 63]) {
-        FS_CUDA(cudaFuncSetAttribute(gemm_skinny_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-        attr_set[device & 63] = true;
-    }
     cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3(sms);
+    lc.gridDim = dim3(grid);
     lc.blockDim = dim3(kGemmThreads);
     lc.dynamicSmemBytes = smem;
     lc.stream = static_cast<cudaStream_t>(stream);
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = prm.splits;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     lc.attrs = attr;
-    lc.numAttrs = 1;
-    FS_CUDA(cudaLaunchKernelEx(&lc, gemm_skinny_kernel, mw, mx, prm));
-    // the split-tile reduction (blocks of whole tiles exit at once)
-    {
-        cudaLaunchConfig_t lr = lc;
-        lr.gridDim = dim3(prm.tiles, (rows + kRedRows - 1) / kRedRows);
-        lr.blockDim = dim3(kTileM);
-        lr.dynamicSmemBytes = 0;
-        FS_CUDA(cudaLaunchKernelEx(&lr, gemm_reduce_kernel, prm, (int32_t)sms));
-    }
+    lc.numAttrs = 2;
+    if (w_layout == 0)
+        FS_CUDA(cudaLaunchKernelEx(&lc, gemm_skinny_kernel<1, false>, mw, mx, prm));
+    else if (group == 1)
+        FS_CUDA(cudaLaunchKernelEx(&lc, gemm_skinny_kernel<1, true>, mw, mx, prm));
+    else
+        FS_CUDA(cudaLaunchKernelEx(&lc, gemm_skinny_kernel<2, true>, mw, mx, prm));
     return FS_OK;
 }

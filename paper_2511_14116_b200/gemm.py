@@ -33,31 +33,69 @@ def interleave_gate_up(w_gate: torch.Tensor, w_up: torch.Tensor) -> torch.Tensor
     return torch.cat([g, u], dim=2).reshape(K, 2 * C).contiguous()
 
 
+def _sm_count(device=None) -> int:
+    return torch.cuda.get_device_properties(device if device is not None else
+                                            torch.cuda.current_device()).multi_processor_count
+
+
 class PackedWeight:
     """A [K, N] weight pre-packed (once, at load) into the GEMM's streaming
     order: one 16 KB block per (128-column tile t, 64-row k-step s), blocks
-    ordered [t][s], each block in the tcgen05 canonical no-swizzle MN-major
-    layout [k-group 8][m-group 16][k 8][m 8].  The kernel moves a block with
-    ONE 1-D bulk copy straight into the UMMA operand layout, and a CTA's
-    stream-K range is one contiguous region of HBM."""
+    ordered [group][s][g] with t = group * G + g.  A block is W^T's tile as
+    the UMMA K-major SWIZZLE_128B A operand, as is: 128 rows (output
+    columns) of 64 k x bf16 = 128 B, 16-byte chunk c of row f stored at
+    chunk c ^ (f % 8).  A CTA owns a column group and a k-range of it, which
+    is ONE contiguous region of HBM, moved in 32 KB bulk copies.
 
-    def __init__(self, w: torch.Tensor):
+    G (tiles per CTA) is 1, or 2 when the tiles outnumber the SMs (then a
+    group's step is 2 tiles x 16 KB, still one 32 KB copy)."""
+
+    def __init__(self, w: torch.Tensor, group: int = None):
         K, n = w.shape
         if n % 128 or K % 64:
             raise ValidationError("packed weights need N % 128 == 0 and K % 64 == 0")
-        self.K, self.N = K, n
-        blocks = w.reshape(K // 64, 8, 8, n // 128, 16, 8)       # s, kg, kr, t, mg, mc
-        self.panels = blocks.permute(3, 0, 1, 4, 2, 5).contiguous()  # t, s, kg, mg, kr, mc
+        tiles = n // 128
+        if group is None:
+            group = 2 if tiles > _sm_count(w.device) and tiles % 2 == 0 else 1
+        if group not in (1, 2) or tiles % group:
+            raise ValidationError(f"bad column group {group} for {tiles} tiles")
+        self.K, self.N, self.group = K, n, group
+        # w[k, col]: k = (s, ch, e), col = (grp, g, f)
+        b = w.reshape(K // 64, 8, 8, tiles // group, group, 128)    # s ch e grp g f
+        b = b.permute(3, 0, 4, 5, 1, 2)                             # grp s g f ch e
+        f, sw = _swizzle_index(w.device)
+        self.panels = b[:, :, :, f, sw].contiguous()
+
+    @classmethod
+    def empty(cls, K: int, n: int, device, group: int = 1) -> "PackedWeight":
+        """Uninitialised panels of a [K, n] weight (filled by block copies:
+        failover adoption, hybrid.HybridDecodeRank.adopt)."""
+        if n % (128 * group) or K % 64:
+            raise ValidationError("packed weights need N % 128 == 0 and K % 64 == 0")
+        self = cls.__new__(cls)
+        self.K, self.N, self.group = K, n, group
+        self.panels = torch.empty((n // (128 * group), K // 64, group, 128, 8, 8),
+                                  dtype=torch.bfloat16, device=device)
+        return self
 
     def unpack(self) -> torch.Tensor:
-        return self.panels.permute(1, 2, 4, 0, 3, 5).reshape(self.K, self.N)
+        f, sw = _swizzle_index(self.panels.device)
+        b = self.panels[:, :, :, f, sw]                             # the swizzle is an involution
+        return b.permute(1, 4, 5, 0, 2, 3).reshape(self.K, self.N)
+
+
+def _swizzle_index(device):
+    f = torch.arange(128, device=device)
+    return f[:, None], torch.arange(8, device=device)[None, :] ^ (f[:, None] & 7)
 
 
 class SkinnyGemm:
-    """Workspace + semaphores for ``fs_gemm_skinny`` on one device (shared
-    by all projections of an engine; launches are stream-ordered)."""
+    """Launcher of ``fs_gemm_skinny`` on one device (shared by all
+    projections of an engine; launches are stream-ordered).  The ABI's
+    workspace / semaphore arguments are reserved (split tiles are reduced
+    over distributed shared memory); minimal buffers are passed."""
 
-    def __init__(self, max_n: int, device=None):
+    def __init__(self, max_n: int = 0, device=None):
         self.device = torch.device(device if device is not None else "cuda")
         self.index = self.device.index if self.device.index is not None \
             else torch.cuda.current_device()
@@ -66,7 +104,7 @@ class SkinnyGemm:
             raise ValidationError("cannot size the GEMM workspace")
         self.max_n = max_n
         self.ws = torch.empty(floats, dtype=torch.float32, device=self.device)
-        self.sems = torch.zeros(2 * max(1, max_n // 128), dtype=torch.int32, device=self.device)
+        self.sems = torch.zeros(2, dtype=torch.int32, device=self.device)
 
     def __call__(self, x: torch.Tensor, w, out: torch.Tensor,
                  epilogue: int = STORE, res: torch.Tensor = None) -> torch.Tensor:
@@ -79,8 +117,6 @@ class SkinnyGemm:
         Kw, n = (w.K, w.N) if packed else w.shape
         if Kw != K or x.stride(1) != 1 or wt.stride(-1) != 1 or out.stride(1) != 1:
             raise ValidationError("skinny GEMM: shape / layout mismatch")
-        if n > self.max_n:
-            raise ValidationError(f"N={n} exceeds the workspace sized for {self.max_n}")
         if epilogue == RESIDUAL and res is None:
             res = out
         stream = N.C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
@@ -91,7 +127,7 @@ class SkinnyGemm:
             rs = res[r0:r0 + r] if res is not None else None
             N.check(N.lib.fs_gemm_skinny(
                 N.ptr(xs), x.stride(0), r, K, N.ptr(wt), 128 if packed else wt.stride(0),
-                1 if packed else 0, n, N.ptr(os), out.stride(0),
+                w.group if packed else 0, n, N.ptr(os), out.stride(0),
                 N.ptr(rs), res.stride(0) if res is not None else 0, epilogue, N.ptr(self.ws),
                 ws_floats, N.ptr(self.sems), self.index, stream), "fs_gemm_skinny")
         return out

@@ -115,7 +115,7 @@ class HybridDecodeRank:
 
     def __init__(self, model: ModelSpec, owner, rank: int, routing, batch: int, capacity: int,
                  device=None, seed: int = 0, group=None, page_order: str = "contiguous",
-                 config: int = 0, mlp: bool = False, shard_owner=None, gemm: str = "cublas",
+                 config: int = 0, mlp: bool = False, shard_owner=None, gemm: str = "tcgen05",
                  request_capacity=None, exchange: str = "nccl", exchange_elems: int = None,
                  reserve_pages: int = 0):
         if model.head_dim != N.HEAD_DIM:
@@ -347,6 +347,8 @@ class HybridDecodeRank:
         """Slot ``j`` of ``layer`` in the fused weights as the 4 parts of a
         canonical head piece (hostmirror.WeightLayout), in piece order:
         [(address, row pitch, row bytes, rows, offset in the piece)]."""
+        if self.gemm == "tcgen05":
+            return self._head_parts_packed(layer, j, wqkv, wo, S)
         wqkv = self.wqkv if wqkv is None else wqkv
         wo = self.wo if wo is None else wo
         S = self.n_slots if S is None else S
@@ -360,9 +362,50 @@ class HybridDecodeRank:
                 (base + (qw + (S + j) * hd) * 2, rw * 2, hd * 2, hid, qb + kb),   # Wv
                 (o_addr, qpk * hd * hid * 2, qpk * hd * hid * 2, 1, qb + 2 * kb)]  # Wo
 
+    # packed weights (gemm.PackedWeight, one column group): 16 KB blocks,
+    # a 128-column tile's blocks contiguous over k.  A head piece is [Wq
+    # panels (qpk tiles) | Wk panel | Wv panel | Wo: per output tile, the
+    # head's 2 qpk k-step blocks]; a shard piece is [gate/up panels (w/64
+    # interleaved tiles) | Wd: per output tile, the shard's w/64 k-step
+    # blocks] -- the same bytes as the row-major pieces, in the layout the
+    # GEMM streams, so adoption is plain block copies.
+    _BLK = 16384
+
+    def _head_parts_packed(self, layer: int, j: int, p_qkv=None, p_o=None, S=None):
+        p_qkv = self.p_qkv if p_qkv is None else p_qkv
+        p_o = self.p_o if p_o is None else p_o
+        S = self.n_slots if S is None else S
+        qpk, hid, B = self.qpk, self.model.hidden_dim, self._BLK
+        q, o = p_qkv[layer], p_o[layer]
+        if q.group != 1 or o.group != 1:
+            raise ValidationError("failover needs one-tile column groups")
+        panel = (hid // 64) * B
+        qb, base = qpk * panel, q.panels.data_ptr()
+        nk_o = o.K // 64
+        return [(base + j * qb, qb, qb, 1, 0),                                  # Wq
+                (base + (S * qpk + j) * panel, panel, panel, 1, qb),             # Wk
+                (base + (S * qpk + S + j) * panel, panel, panel, 1, qb + panel),  # Wv
+                (o.panels.data_ptr() + j * 2 * qpk * B, nk_o * B, 2 * qpk * B, hid // 128,
+                 qb + 2 * panel)]                                                # Wo
+
+    def _shard_parts_packed(self, layer: int, k: int, p_gu=None, p_d=None):
+        p_gu = self.p_gu if p_gu is None else p_gu
+        p_d = self.p_d if p_d is None else p_d
+        hid, B = self.model.hidden_dim, self._BLK
+        gu, d = p_gu[layer], p_d[layer]
+        if gu.group != 1 or d.group != 1:
+            raise ValidationError("failover needs one-tile column groups")
+        tw = (self.model.ffn_intermediate_dim // self.num_shards) // 64
+        panel = (hid // 64) * B
+        return [(gu.panels.data_ptr() + k * tw * panel, tw * panel, tw * panel, 1, 0),  # Wg|Wu
+                (d.panels.data_ptr() + k * tw * B, (d.K // 64) * B, tw * B, hid // 128,
+                 tw * panel)]                                                     # Wd
+
     def _shard_parts(self, layer: int, k: int, w_gu=None, w_d=None):
         """Local FFN shard ``k`` of ``layer`` as the parts of a canonical
         shard piece ``[Wg | Wu | Wd]`` (same tuple format)."""
+        if self.gemm == "tcgen05":
+            return self._shard_parts_packed(layer, k, w_gu, w_d)
         w_gu = self.w_gu if w_gu is None else w_gu
         w_d = self.w_d if w_d is None else w_d
         hid = self.model.hidden_dim
@@ -395,8 +438,6 @@ class HybridDecodeRank:
         layer the head ids to publish) and its FFN shards.  One launch
         (D2H over PCIe into the mapped store); returns bytes written."""
         from .hostmirror import SegmentCopy
-        if self.gemm != "cublas":
-            raise ValidationError("publish_weights needs the cuBLAS weight layout")
         lay = store.layout
         seg = SegmentCopy()
         for layer in range(self.model.num_layers):
@@ -440,8 +481,6 @@ class HybridDecodeRank:
         piece} (the K7 staging buffer).  Returns the new items (their KV is
         restored by the caller).  The step graph must be captured again."""
         from .hostmirror import SegmentCopy
-        if self.gemm != "cublas":
-            raise ValidationError("adopt needs the cuBLAS weight layout")
         old_work = self.work
         work = RankWork.build(np.asarray(owner, dtype=np.int32), self.rank, routing, self.batch)
         new_shards = sorted(s_ for s_, g in enumerate(shard_owner) if g == self.rank) \
@@ -456,8 +495,14 @@ class HybridDecodeRank:
         S = work.n_slots
         rw = S * (qpk + 2) * hd
         dev = self.device
-        wqkv = torch.zeros((L, hid, rw), dtype=torch.bfloat16, device=dev)
-        wo = torch.zeros((L, S * qpk * hd, hid), dtype=torch.bfloat16, device=dev)
+        packed = self.gemm == "tcgen05"
+        if packed:
+            from .gemm import PackedWeight
+            wqkv = [PackedWeight.empty(hid, rw, dev) for _ in range(L)]
+            wo = [PackedWeight.empty(S * qpk * hd, hid, dev) for _ in range(L)]
+        else:
+            wqkv = torch.zeros((L, hid, rw), dtype=torch.bfloat16, device=dev)
+            wo = torch.zeros((L, S * qpk * hd, hid), dtype=torch.bfloat16, device=dev)
         seg = SegmentCopy()
         for layer in range(L):
             old_heads = old_work.slot_heads[layer]
@@ -474,8 +519,12 @@ class HybridDecodeRank:
         if self.mlp:
             shards = sorted(s_ for s_, g in enumerate(shard_owner) if g == self.rank)
             C = len(shards) * (self.model.ffn_intermediate_dim // self.num_shards)
-            w_gu = torch.zeros((L, hid, 2 * C), dtype=torch.bfloat16, device=dev)
-            w_d = torch.zeros((L, C, hid), dtype=torch.bfloat16, device=dev)
+            if packed:
+                w_gu = [PackedWeight.empty(hid, 2 * C, dev) for _ in range(L)]
+                w_d = [PackedWeight.empty(C, hid, dev) for _ in range(L)]
+            else:
+                w_gu = torch.zeros((L, hid, 2 * C), dtype=torch.bfloat16, device=dev)
+                w_d = torch.zeros((L, C, hid), dtype=torch.bfloat16, device=dev)
             for layer in range(L):
                 for k, sh in enumerate(shards):
                     new_parts = self._shard_parts(layer, k, w_gu=w_gu, w_d=w_d)
@@ -492,9 +541,16 @@ class HybridDecodeRank:
         torch.cuda.current_stream(dev).synchronize()
         fresh = self.cache.adopt(work)
         self.work, self.n_slots = work, S
-        self.wqkv, self.wo = wqkv, wo
+        if packed:
+            self.p_qkv, self.p_o = wqkv, wo
+        else:
+            self.wqkv, self.wo = wqkv, wo
         if self.mlp:
-            self.w_gu, self.w_d, self.shards = w_gu, w_d, shards
+            if packed:
+                self.p_gu, self.p_d = w_gu, w_d
+            else:
+                self.w_gu, self.w_d = w_gu, w_d
+            self.shards = shards
             self.ffn_cols = ffn_columns(self.model, shard_owner, self.rank)
             C = len(self.ffn_cols)
             self.h = torch.empty((self.batch, 2 * C), dtype=torch.bfloat16, device=dev)
@@ -515,13 +571,12 @@ class HybridDecodeRank:
                 "fs_kv_backup_tokens")
 
     def launches_per_step(self) -> int:
-        """Our kernel launches per step: the fused decode launch per layer,
-        plus the swiglu launch per layer with the MLP (cuBLAS GEMMs), or the
-        decode + 4 tcgen05 GEMMs per layer, each a GEMM launch and its
-        split-tile reduction launch (gemm="tcgen05")."""
+        """Our kernel launches per step: the fused decode launch per layer
+        plus its 4 tcgen05 GEMM launches (2 without the MLP; gemm="tcgen05"),
+        or the decode + swiglu launches per layer (cuBLAS GEMMs)."""
         has_mlp = self.mlp and len(self.ffn_cols)
         if self.gemm == "tcgen05":
-            n = self.model.num_layers * (1 + 2 * (4 if has_mlp else 2))
+            n = self.model.num_layers * (1 + (4 if has_mlp else 2))
         else:
             n = self.model.num_layers * (2 if has_mlp else 1)
         if self.xchg is not None:  # one fs_ar_residual per exchange

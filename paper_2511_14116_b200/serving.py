@@ -238,7 +238,8 @@ class HybridServingRank(HybridDecodeRank):
                          config=config, mlp=mlp, shard_owner=shard_owner,
                          request_capacity=cap, exchange=exchange,
                          exchange_elems=int(max_tokens) * model.hidden_dim,
-                         reserve_pages=reserve_pages)
+                         reserve_pages=reserve_pages,
+                         gemm="cublas")  # iterations of ~2k tokens: compute-bound library GEMMs
         self.request_capacity = cap
         self.max_tokens = int(max_tokens)
         self._derive()

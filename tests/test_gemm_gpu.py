@@ -76,16 +76,20 @@ def test_validation():
         SkinnyGemm(128)(x, w, out)
 
 
-@pytest.mark.parametrize("K,N,epi", [(4096, 1280, 0), (1024, 4096, 1), (2048, 896, 2)])
-def test_packed_panels_match_row_major(K, N, epi):
+@pytest.mark.parametrize("K,N,epi,group", [(4096, 1280, 0, 1), (1024, 4096, 1, 1), (2048, 896, 2, 1),
+                                           (4096, 1280, 0, 2), (1024, 4096, 1, 2), (2048, 1024, 2, 2),
+                                           (8192, 38912, 2, None)])
+def test_packed_panels_match_row_major(K, N, epi, group):
     from paper_2511_14116_b200.gemm import PackedWeight, SkinnyGemm, interleave_gate_up
     g = torch.Generator(device="cuda").manual_seed(K + N)
     x = torch.randn((64, K), device="cuda", generator=g).to(torch.bfloat16)
     w = (torch.randn((K, N), device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
     if epi == 2:
         w = interleave_gate_up(w[:, :N // 2], w[:, N // 2:])
-    pw = PackedWeight(w)
+    pw = PackedWeight(w, group)
     assert torch.equal(pw.unpack(), w)
+    if group is None:  # more 128-column tiles than SMs: two tiles per CTA
+        assert pw.group == 2
     n_out = N // 2 if epi == 2 else N
     base = torch.randn((64, n_out), device="cuda", generator=g).to(torch.bfloat16)
     a, b = base.clone(), base.clone()
@@ -93,4 +97,32 @@ def test_packed_panels_match_row_major(K, N, epi):
     gemm(x, w, a, epi)
     gemm(x, pw, b, epi)
     torch.cuda.synchronize()
-    assert torch.equal(a, b)
+    if pw.group == 1:  # same launch plan as the row-major W: same bits
+        assert torch.equal(a, b)
+    assert int(gemm.sems.abs().sum()) == 0
+    ref = _ref(x, w)
+    if epi == 2:
+        g_, u_ = ref.view(64, -1, 2, 64)[:, :, 0].reshape(64, -1), ref.view(64, -1, 2, 64)[:, :, 1].reshape(64, -1)
+        ref = torch.nn.functional.silu(g_) * u_
+    elif epi == 1:
+        ref = ref + base.float()
+    _close(b, ref)
+
+
+@pytest.mark.parametrize("rows", [1, 3, 17, 64])
+def test_split_reduction_rows(rows):
+    """Small row counts with many k-splits per tile (QKV-like: 10 tiles over
+    K = 8192): row slices of the in-grid reduction may be empty."""
+    from paper_2511_14116_b200.gemm import RESIDUAL, PackedWeight, SkinnyGemm
+    g = torch.Generator(device="cuda").manual_seed(rows)
+    x = torch.randn((rows, 8192), device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn((8192, 1280), device="cuda", generator=g) / 90.0).to(torch.bfloat16)
+    base = torch.randn((rows, 1280), device="cuda", generator=g).to(torch.bfloat16)
+    out = base.clone()
+    gemm = SkinnyGemm(1280)
+    for _ in range(3):  # counters reset between launches
+        out.copy_(base)
+        gemm(x, PackedWeight(w), out, RESIDUAL)
+    torch.cuda.synchronize()
+    _close(out, base.float() + _ref(x, w))
+    assert int(gemm.sems.abs().sum()) == 0

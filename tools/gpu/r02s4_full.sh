@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
+tail -30 gpurun_out/pytest_gpu.log
