@@ -52,9 +52,11 @@ constexpr int kStageX = 2 * kBlockX;           // 16 KB
 constexpr int kStageBytes = kStageW + kStageX;
 constexpr int kGemmThreads = 192;
 constexpr int kPrefetchA = 3;   // W stages issued before the PDL wait
-constexpr int kMaxGroup = 2;
 constexpr int kMaxSplits = 8;                 // portable cluster size
-constexpr int kOtPitch = kMaxGroup * kTileM + 4;  // fp32 output-tile row pitch
+// fp32 output tile [64][G * 128 + 4] (over the drained stage ring) and the
+// split reduction's receive area [S][ceil(rows / S)][same pitch] after it
+__host__ __device__ constexpr int ot_pitch(int G) { return G * kTileM + 4; }
+constexpr int kRcvOff = 69632;  // >= 64 rows x ot_pitch(2) x 4 B, 1 KB aligned
 
 
 enum GemmEpilogue { EPI_STORE = 0, EPI_RESIDUAL = 1, EPI_SWIGLU = 2 };
@@ -168,73 +170,111 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-__device__ __forceinline__ float silu(float g) { return g / (1.f + __expf(-g)); }
+__device__ __forceinline__ float silu(float g) { return __fdividef(g, 1.f + __expf(-g)); }
 
 // Output writer shared by both paths: rows [0, nr) of the CTA's output
 // region (global rows row0 + r) in 16-byte chunks, consecutive threads on
-// consecutive chunks (coalesced), residual loads of a round issued before
-// any use.  val(r, col, v) fills v[8] with the fp32 GEMM values of CTA-local
-// columns col..col+7 (col in [0, 128 G)).  STORE / RESIDUAL: chunk = 8
-// output columns; SWIGLU: chunk = 8 activations from gate col and up col+64.
-template <int G, typename Val>
-__device__ __forceinline__ void gemm_write(const GemmParams &p, int grp, int row0, int nr,
-                                           int t, Val val) {
-    const bool swiglu = p.epilogue == EPI_SWIGLU, resid = p.epilogue == EPI_RESIDUAL;
-    const int cpr = (swiglu ? 8 : 16) * G;  // chunks per row
+// consecutive chunks (coalesced).  val(r, col, v) fills v[8] with the fp32
+// GEMM values of CTA-local columns col..col+7 (col in [0, 128 G)), read
+// from shared memory.  STORE / RESIDUAL: chunk = 8 output columns; SWIGLU:
+// chunk = 8 activations from gate col and up col + 64.  One epilogue kind
+// per instantiation and a rolled loop: this code runs once per CTA, so it
+// is kept small (cold instruction fetch, not arithmetic, bounds it);
+// residual rows are prefetched 4 chunks at a time.
+template <int G, int EPI, typename Val>
+__device__ __noinline__ void gemm_write_epi(const GemmParams &p, int grp, int row0, int nr,
+                                            int t, Val val, bool live) {
+    constexpr int cpr = (EPI == EPI_SWIGLU ? 8 : 16) * G;  // chunks per row
     const int total = nr * cpr;
-    constexpr int U = 4;
-    for (int base = 0; base < total; base += U * 128) {
-        // every load of the round first (residual rows, values), then use
-        uint4 rv[U];
-        float v[U][8], w[U][8];
+#pragma unroll 1
+    for (int base = t; base < total; base += 4 * 128) {
+        uint4 rv[4];
+        if (EPI == EPI_RESIDUAL) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int idx = base + u * 128 + t;
-            rv[u] = make_uint4(0, 0, 0, 0);
-            if (idx < total) {
+            for (int u = 0; u < 4; ++u) {
+                const int idx = base + u * 128;
                 const int r = idx / cpr, ch = idx % cpr;
-                if (swiglu) {
-                    const int g = ch >> 3, a = (ch & 7) * 8;
-                    val(r, g * kTileM + a, v[u]);
-                    val(r, g * kTileM + 64 + a, w[u]);
-                } else {
-                    val(r, ch * 8, v[u]);
-                    if (resid)
-                        rv[u] = *reinterpret_cast<const uint4 *>(
-                            p.res + (int64_t)(row0 + r) * p.ld_res + (int64_t)(grp * G) * kTileM + ch * 8);
-                }
+                rv[u] = idx < total ? *reinterpret_cast<const uint4 *>(
+                                          p.res + (int64_t)(row0 + r) * p.ld_res +
+                                          (int64_t)(grp * G) * kTileM + ch * 8)
+                                    : make_uint4(0, 0, 0, 0);
             }
         }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int idx = base + u * 128 + t;
+#pragma unroll 1
+        for (int u = 0; u < 4; ++u) {
+            const int idx = base + u * 128;
             if (idx >= total) break;
             const int r = idx / cpr, ch = idx % cpr;
+            float v[8];
             uint4 o;
-            if (swiglu) {
+            if (EPI == EPI_SWIGLU) {
                 const int g = ch >> 3, a = (ch & 7) * 8;
-                o.x = pack_bf16(silu(v[u][0]) * w[u][0], silu(v[u][1]) * w[u][1]);
-                o.y = pack_bf16(silu(v[u][2]) * w[u][2], silu(v[u][3]) * w[u][3]);
-                o.z = pack_bf16(silu(v[u][4]) * w[u][4], silu(v[u][5]) * w[u][5]);
-                o.w = pack_bf16(silu(v[u][6]) * w[u][6], silu(v[u][7]) * w[u][7]);
-                *reinterpret_cast<uint4 *>(p.out + (int64_t)(row0 + r) * p.ld_out +
-                                           (int64_t)(grp * G + g) * 64 + a) = o;
+                float w[8];
+                val(r, g * kTileM + a, v);
+                val(r, g * kTileM + 64 + a, w);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] = silu(v[i]) * w[i];
+                o = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]),
+                               pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+                if (live)
+                    *reinterpret_cast<uint4 *>(p.out + (int64_t)(row0 + r) * p.ld_out +
+                                               (int64_t)(grp * G + g) * 64 + a) = o;
             } else {
-                if (resid) {
-                    const uint32_t q[4] = {rv[u].x, rv[u].y, rv[u].z, rv[u].w};
+                val(r, ch * 8, v);
+                if (EPI == EPI_RESIDUAL) {
+                    uint4 q = rv[0];
+                    if (u == 1) q = rv[1];
+                    if (u == 2) q = rv[2];
+                    if (u == 3) q = rv[3];
+                    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        v[u][2 * i] += __uint_as_float(q[i] << 16);
-                        v[u][2 * i + 1] += __uint_as_float(q[i] & 0xffff0000u);
+                        v[2 * i] += __uint_as_float(w[i] << 16);
+                        v[2 * i + 1] += __uint_as_float(w[i] & 0xffff0000u);
                     }
                 }
-                o.x = pack_bf16(v[u][0], v[u][1]);
-                o.y = pack_bf16(v[u][2], v[u][3]);
-                o.z = pack_bf16(v[u][4], v[u][5]);
-                o.w = pack_bf16(v[u][6], v[u][7]);
-                *reinterpret_cast<uint4 *>(p.out + (int64_t)(row0 + r) * p.ld_out +
-                                           (int64_t)(grp * G) * kTileM + ch * 8) = o;
+                o = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]),
+                               pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+                if (live)
+                    *reinterpret_cast<uint4 *>(p.out + (int64_t)(row0 + r) * p.ld_out +
+                                               (int64_t)(grp * G) * kTileM + ch * 8) = o;
             }
+        }
+    }
+}
+
+// live == false: the same code with every store off -- run by the idle
+// epilogue warps during the main loop, so the (once per CTA, L2-evicted by
+// the weight stream) epilogue instructions are cached when they are needed
+template <int G, typename Val>
+__device__ __forceinline__ void gemm_write(const GemmParams &p, int grp, int row0, int nr,
+                                           int t, Val val, bool live = true) {
+    if (p.epilogue == EPI_SWIGLU)
+        gemm_write_epi<G, EPI_SWIGLU>(p, grp, row0, nr, t, val, live);
+    else if (p.epilogue == EPI_RESIDUAL)
+        gemm_write_epi<G, EPI_RESIDUAL>(p, grp, row0, nr, t, val, live);
+    else
+        gemm_write_epi<G, EPI_STORE>(p, grp, row0, nr, t, val, live);
+}
+
+// accumulators -> fp32 tile [64][kOt] in shared memory: thread m owns
+// column m (TMEM lane) for all 64 rows (live == false: instruction warm-up)
+template <int G, int kOt>
+__device__ __noinline__ void tile_to_smem(uint32_t tmem, float *ot, int warp, int m, bool live) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            float v[32];
+            if (live) {
+                tmem_ld32(tmem + g * kRowsN + h * 32 + ((uint32_t)(warp * 32) << 16), v);
+            } else {
+#pragma unroll
+                for (int n = 0; n < 32; ++n) v[n] = 0.f;
+            }
+#pragma unroll
+            for (int n = 0; n < 32; ++n)
+                if (live) ot[(h * 32 + n) * kOt + g * kTileM + m] = v[n];
         }
     }
 }
@@ -244,20 +284,20 @@ __device__ __forceinline__ void cluster_sync_all() {
                  "barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// (relaxed: the closing barrier orders no memory, it only keeps source
+// tiles alive until the copies reading them have landed)
+__device__ __forceinline__ void cluster_arrive() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
     uint32_t r;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
     return r;
-}
-
-// (no memory clobber: the tiles are read-only between the two cluster
-// barriers, so the loads of a round may be batched)
-__device__ __forceinline__ float4 ld_dsmem_v4(uint32_t addr) {
-    float4 v;
-    asm("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-        : "r"(addr));
-    return v;
 }
 
 // one lane of the (converged) warp: true on exactly one lane
@@ -276,8 +316,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                        const __grid_constant__ CUtensorMap map_x, const GemmParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte aligned base for the swizzled stages
-    uint8_t *smem = reinterpret_cast<uint8_t *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // (pointer arithmetic on the __shared__ array keeps the state space
+    // known, so tile accesses compile to LDS / STS)
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sbase = smem_u32(smem);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kGemmStages * kStageBytes);
     const uint32_t bar_full = smem_u32(bars);
@@ -292,6 +333,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     constexpr int sps = G == 1 ? 2 : 1;                // k-steps per stage
     const int n_st = (k1 - k0 + sps - 1) / sps;        // >= 1 (splits <= nk)
     constexpr uint32_t tcols = G == 1 ? 64u : 128u;
+    constexpr int kOt = ot_pitch(G);
+    const uint32_t bar_red = bar_acc + 8;
 
     if (warp == 4 && lane == 0) {
         prefetch_tmap(&map_w);
@@ -301,6 +344,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             mbar_init(bar_empty + 8 * s, 1);
         }
         mbar_init(bar_acc, 1);
+        mbar_init(bar_red, 1);
         fence_barrier_init();
         fence_proxy_async();
     }
@@ -315,6 +359,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_fence_after();
     const uint32_t tmem = s_tmem;
     if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 16 + 0] = gtimer();
+
+    // epilogue geometry and value readers (shared by the warm-up and the
+    // live epilogue, so both run the same code)
+    float *ot = reinterpret_cast<float *>(smem);
+    const float *rv = reinterpret_cast<const float *>(smem + kRcvOff);
+    const int nrmax = (p.rows + S - 1) / S;
+    const int r0 = split * p.rows / S, r1 = (split + 1) * p.rows / S, nr = r1 - r0;
+    const auto val_tile = [=](int r, int col, float (&v)[8]) {
+        const float4 *q = reinterpret_cast<const float4 *>(ot + r * kOt + col);
+        const float4 x0 = q[0], x1 = q[1];
+        v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
+        v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+    };
+    const auto val_split = [=](int r, int col, float (&v)[8]) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = 0.f;
+        for (int s0 = 0; s0 < S; ++s0) {  // split order: deterministic
+            const float *src = s0 == split ? ot + (r0 + r) * kOt + col
+                                           : rv + (s0 * nrmax + r) * kOt + col;
+            const float4 x0 = reinterpret_cast<const float4 *>(src)[0];
+            const float4 x1 = reinterpret_cast<const float4 *>(src)[1];
+            v[0] += x0.x; v[1] += x0.y; v[2] += x0.z; v[3] += x0.w;
+            v[4] += x1.x; v[5] += x1.y; v[6] += x1.z; v[7] += x1.w;
+        }
+    };
 
     if (warp == 4) {
         // ---------------- TMA producer ----------------
@@ -408,70 +477,67 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (p.dbg && lane == 0) p.dbg[blockIdx.x * 16 + 2] = gtimer();
     } else {
         // ---------------- epilogue (warps 0-3) ----------------
-        // accumulators -> fp32 tile [64][128 G + 4] over the (drained) stage
-        // ring: thread m owns column m (TMEM lane) for all 64 rows
         const int m = warp * 32 + lane;
+        // instruction warm-up while the main loop streams (no side effects)
+        tile_to_smem<G, kOt>(tmem, ot, warp, m, false);
+        if (S == 1)
+            gemm_write<G>(p, grp, 0, 1, m, val_tile, false);
+        else
+            gemm_write<G>(p, grp, r0, 1, m, val_split, false);
         mbar_wait(bar_acc, 0);
         tc_fence_after();
         grid_dependency_wait();  // out / res: after the previous kernel
         if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 16 + 8] = gtimer();
-        float *ot = reinterpret_cast<float *>(smem);
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                float v[32];
-                tmem_ld32(tmem + g * kRowsN + h * 32 + ((uint32_t)(warp * 32) << 16), v);
-#pragma unroll
-                for (int n = 0; n < 32; ++n) ot[(h * 32 + n) * kOtPitch + g * kTileM + m] = v[n];
-            }
-        }
+        tile_to_smem<G, kOt>(tmem, ot, warp, m, true);
         if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 16 + 3] = gtimer();
         if (S == 1) {
             named_bar_sync(1, 128);
-            gemm_write<G>(p, grp, 0, p.rows, m, [&](int r, int col, float (&v)[8]) {
-                const float4 *q = reinterpret_cast<const float4 *>(ot + r * kOtPitch + col);
-                const float4 x0 = q[0], x1 = q[1];
-                v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
-                v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
-            });
+            gemm_write<G>(p, grp, 0, p.rows, m, val_tile);
         }
     }
     if (S > 1) {
         // ---- split reduction over distributed shared memory: the group's
-        // splits are one thread-block cluster (rank = split).  Each CTA sums
-        // its 1/S slice of the rows over every split's tile, in split order
-        // (deterministic), and writes it; a second cluster barrier keeps
-        // every tile alive until its readers are done ----
+        // splits are one thread-block cluster (rank = split).  After a
+        // cluster barrier (every split's MMAs done, its tile in its shared
+        // memory, every receive barrier armed) each CTA pushes row slice k
+        // of its tile to CTA k with ONE bulk copy (the TMA engine moves it;
+        // no thread waits on DSMEM latency), sums its own slice over the S
+        // tiles in split order (deterministic) and writes it.  The closing
+        // barrier (arrived once a CTA's incoming copies landed) keeps every
+        // source tile alive until its copy is done. ----
+        const uint32_t rcv = sbase + kRcvOff;
+        constexpr uint32_t row_bytes = kOt * 4;
+        if (threadIdx.x == 0)
+            mbar_expect_tx(bar_red, (uint32_t)((S - 1) * nr) * row_bytes);
         __syncwarp();
-        cluster_sync_all();  // all S partial tiles are in shared memory
+        cluster_sync_all();
         if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 16 + 7] = gtimer();
+        if (threadIdx.x == 0) {
+            fence_proxy_async();  // the tile was written with STS
+            for (int k = 0; k < S; ++k) {
+                if (k == split) continue;
+                const int a = k * p.rows / S, b = (k + 1) * p.rows / S;
+                if (b == a) continue;
+                const uint32_t dst = mapa_shared(rcv + (uint32_t)(split * nrmax) * row_bytes, k);
+                const uint32_t mb = mapa_shared(bar_red, k);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes"
+                    " [%0], [%1], %2, [%3];" ::"r"(dst), "r"(sbase + (uint32_t)a * row_bytes),
+                    "r"((uint32_t)(b - a) * row_bytes), "r"(mb)
+                    : "memory");
+            }
+        }
         if (warp < 4) {
-            const int r0 = split * p.rows / S, r1 = (split + 1) * p.rows / S;
-            gemm_write<G>(p, grp, r0, r1 - r0, threadIdx.x, [&](int r, int col, float (&v)[8]) {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) v[i] = 0.f;
-                const uint32_t off = sbase + (uint32_t)(((r0 + r) * kOtPitch + col) * 4);
-                for (int sb = 0; sb < S; sb += 4) {  // 4 splits' loads in flight
-                    float4 x[4][2];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        if (sb + i < S) {
-                            const uint32_t q = mapa_shared(off, (uint32_t)(sb + i));
-                            x[i][0] = ld_dsmem_v4(q);
-                            x[i][1] = ld_dsmem_v4(q + 16);
-                        }
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)  // split order: deterministic
-                        if (sb + i < S) {
-                            v[0] += x[i][0].x; v[1] += x[i][0].y; v[2] += x[i][0].z; v[3] += x[i][0].w;
-                            v[4] += x[i][1].x; v[5] += x[i][1].y; v[6] += x[i][1].z; v[7] += x[i][1].w;
-                        }
-                }
-            });
+            mbar_wait(bar_red, 0);
+            if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 16 + 9] = gtimer();
+            cluster_arrive();
+            if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 16 + 11] = gtimer();
+            gemm_write<G>(p, grp, r0, nr, threadIdx.x, val_split);
+        } else {
+            cluster_arrive();
         }
         if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 16 + 10] = gtimer();
-        cluster_sync_all();  // peers are done reading this CTA's tile
+        cluster_wait();  // every copy out of this CTA's tile has landed
     }
     if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 16 + 4] = gtimer();
     tc_fence_before();
@@ -519,6 +585,9 @@ static int make_map(CUtensorMap *map, const void *ptr, int rank, const cuuint64_
 static unsigned long long *g_gemm_dbg = nullptr;  // fs_gemm_debug_timestamps
 
 static size_t gemm_smem() {
+    static_assert(kRcvOff + 70 * ot_pitch(1) * 4 <= kGemmStages * kStageBytes &&
+                      kRcvOff + 64 * ot_pitch(2) * 4 <= kGemmStages * kStageBytes,
+                  "tile + receive area must fit in the stage ring");
     return 1024 + (size_t)kGemmStages * kStageBytes + 8 * 16;
 }
 
