@@ -1,6 +1,6 @@
 """One C3 (Llama-3-70B-shaped, B=64, ctx 4096) decode step of one rank of a
 hybrid(8) / on-demand-shrunk world, for ncu launch lists and graph timing:
-python tools/c3_step.py --world 8 --rank 0 [--gemm cublas|tcgen05] [--steps 2]"""
+python tools/c3_step.py --world 8 --rank 0 [--gemm tcgen05|cublas] [--steps 2]"""
 import argparse, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -11,7 +11,7 @@ from paper_2511_14116_b200.recovery import plan_weight_recovery
 ap = argparse.ArgumentParser()
 ap.add_argument("--world", type=int, default=8)
 ap.add_argument("--rank", type=int, default=0)
-ap.add_argument("--gemm", default="cublas")
+ap.add_argument("--gemm", default="tcgen05")
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--time", action="store_true", help="graph-time the step instead")
 ap.add_argument("--model", default="70b")
