@@ -316,21 +316,25 @@ typedef struct fs_copy_seg {
 int fs_copy_segments(const fs_copy_seg *segs, const int64_t *row_off, int32_t n_segs,
                      int32_t ctas, void *stream);
 
-/* Skinny weight-streaming GEMM of the decode step (tcgen05.mma + TMA,
- * stream-K over (128-column tile, 64-k) units, persistent grid):
+/* Skinny weight-streaming GEMM of the decode step (tcgen05.mma + TMA):
  *   STORE    (0): out[n, c]  = sum_k x[n, k] W[k, c]
  *   RESIDUAL (1): out[n, c]  = res[n, c] + sum_k x[n, k] W[k, c]  (out may == res)
  *   SWIGLU   (2): out[n, 64t+j] = silu(g) * u with g, u the columns 128t+j and
  *                 128t+64+j of x.W (gate/up interleaved in 64-column blocks)
- * x: bf16 [rows <= 64][K] (row stride ld_x), W: bf16 [K][N] (row stride ld_w,
- * w_layout 0) or packed in 128-column panels [N/128][K][128] (w_layout 1:
- * every 64 x 128 slice the kernel streams is one contiguous 16 KB block),
- * K % 64 == 0, N % 128 == 0.  workspace: >= fs_gemm_workspace_floats fp32
- * (the fp32 partials of split tiles); sems: 2*N/128 int32 (reserved: the
- * split tiles are summed by a second, PDL-launched kernel, so no in-grid
- * semaphores are used; must be non-null).  Two launches on `stream`: the
- * GEMM (programmatic dependent launch: W prefetch overlaps the previous
- * kernel) and the split-tile reduction. */
+ * Replaces the projection matmuls of refexec.py:287-307 (q/k/v, o, gated
+ * FFN; _ffn_partial refexec.py:106-108) for the decode batch.
+ * x: bf16 [rows <= 64][K] (row stride ld_x), W: bf16 [K][N] row-major (row
+ * stride ld_w, w_layout 0) or pre-packed (gemm.PackedWeight): w_layout 1 =
+ * 16 KB UMMA-canonical K-major SWIZZLE_128B blocks per (128-column tile,
+ * 64-k step) ordered [tile][step]; w_layout 2 = the same blocks for pairs of
+ * tiles, ordered [pair][step][tile] (used when the tiles outnumber the SMs).
+ * K % 64 == 0, N % 128 == 0; out / res 16-byte aligned with row strides
+ * that are multiples of 8.  One launch per call: grid = column groups x S
+ * k-splits <= SMs, each split group a thread-block cluster whose partial
+ * tiles are summed over distributed shared memory in split order
+ * (deterministic); programmatic dependent launch (the first weight stages
+ * are fetched while the previous kernel drains).  workspace / sems are
+ * reserved (must be non-null; fs_gemm_workspace_floats returns 1). */
 int64_t fs_gemm_workspace_floats(int device, int32_t N, int32_t epilogue);
 int fs_gemm_skinny(const void *x, int64_t ld_x, int32_t rows, int32_t K, const void *w,
                    int64_t ld_w, int32_t w_layout, int32_t N, void *out, int64_t ld_out, const void *res,
