@@ -389,7 +389,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = s_tmem;
-    if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 16 + 0] = gtimer();
+    if (p.dbg && threadIdx.x == 0) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        p.dbg[blockIdx.x * 16 + 0] = gtimer();
+        p.dbg[blockIdx.x * 16 + 12] = smid;
+    }
 
     // epilogue geometry and value readers.  The warm-up pass runs the same
     // reader types over `dummy` (a never-written 1 KB of shared memory), so

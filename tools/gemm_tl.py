@@ -26,6 +26,9 @@ for K, Nc in zip(args[0::2], args[1::2]):
     d = dbg.view(1024, 16).cpu().numpy().astype(np.int64)
     d = d[d[:, 0] > 0]
     t0 = d[:, 0].min()
+    sm = d[:, 12]
+    print(f"  distinct SMs {len(set(sm.tolist()))} for {len(d)} CTAs (max CTAs on one SM "
+          f"{max(np.bincount(sm)) if len(sm) else 0})")
     print(f"K {K} N {Nc}: {len(d)} CTAs, event {s.elapsed_time(e)*1e3:.1f} us; span {(d[:, 4].max() - t0)/1e3:.1f} us")
     for name, a, b in (("start spread", None, 0), ("start->pdl wait", 0, 5), ("pdl wait", 5, 6),
                        ("start->first stage", 0, 1), ("first stage->MMA done", 1, 2),
