@@ -181,11 +181,32 @@ __device__ __forceinline__ float silu(float g) { return __fdividef(g, 1.f + __ex
 // per instantiation and a rolled loop: this code runs once per CTA, so it
 // is kept small (cold instruction fetch, not arithmetic, bounds it);
 // residual rows are prefetched 4 chunks at a time.
+// 16-byte global store / load with explicit state space (gemm_write_epi is
+// a separate function: generic pointers there compiled to generic ST / LD
+// that re-read the parameter block from the stack after every store)
+__device__ __forceinline__ void stg128(void *ptr, uint4 v) {
+    asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(ptr), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w));
+}
+
+__device__ __forceinline__ uint4 ldg128(const void *ptr) {
+    uint4 v;
+    asm volatile("ld.global.cg.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(ptr));
+    return v;
+}
+
 template <int G, int EPI, typename Val>
-__device__ __noinline__ void gemm_write_epi(const GemmParams &p, int grp, int row0, int nr,
-                                            int t, Val val, bool live) {
+__device__ __noinline__ void gemm_write_epi(__nv_bfloat16 *out, int64_t ld_out,
+                                            const __nv_bfloat16 *res, int64_t ld_res, int grp,
+                                            int row0, int nr, int t, Val val, bool live,
+                                            unsigned long long *stamps) {
     constexpr int cpr = (EPI == EPI_SWIGLU ? 8 : 16) * G;  // chunks per row
     const int total = nr * cpr;
+    const bool stamp = live && stamps && t == 0;
+    if (stamp) stamps[13] = gtimer();
+    int it = 0;
 #pragma unroll 1
     for (int base = t; base < total; base += 4 * 128) {
         uint4 rv[4];
@@ -194,9 +215,8 @@ __device__ __noinline__ void gemm_write_epi(const GemmParams &p, int grp, int ro
             for (int u = 0; u < 4; ++u) {
                 const int idx = base + u * 128;
                 const int r = idx / cpr, ch = idx % cpr;
-                rv[u] = idx < total ? *reinterpret_cast<const uint4 *>(
-                                          p.res + (int64_t)(row0 + r) * p.ld_res +
-                                          (int64_t)(grp * G) * kTileM + ch * 8)
+                rv[u] = idx < total ? ldg128(res + (int64_t)(row0 + r) * ld_res +
+                                             (int64_t)(grp * G) * kTileM + ch * 8)
                                     : make_uint4(0, 0, 0, 0);
             }
         }
@@ -217,10 +237,10 @@ __device__ __noinline__ void gemm_write_epi(const GemmParams &p, int grp, int ro
                 o = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]),
                                pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
                 if (live)
-                    *reinterpret_cast<uint4 *>(p.out + (int64_t)(row0 + r) * p.ld_out +
-                                               (int64_t)(grp * G + g) * 64 + a) = o;
+                    stg128(out + (int64_t)(row0 + r) * ld_out + (int64_t)(grp * G + g) * 64 + a, o);
             } else {
                 val(r, ch * 8, v);
+                if (stamp && it++ == 0) stamps[14] = gtimer();
                 if (EPI == EPI_RESIDUAL) {
                     uint4 q = rv[0];
                     if (u == 1) q = rv[1];
@@ -236,21 +256,33 @@ __device__ __noinline__ void gemm_write_epi(const GemmParams &p, int grp, int ro
                 o = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]),
                                pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
                 if (live)
-                    *reinterpret_cast<uint4 *>(p.out + (int64_t)(row0 + r) * p.ld_out +
-                                               (int64_t)(grp * G) * kTileM + ch * 8) = o;
+                    stg128(out + (int64_t)(row0 + r) * ld_out + (int64_t)(grp * G) * kTileM + ch * 8, o);
             }
         }
     }
+    if (stamp) stamps[15] = gtimer();
+}
+
+// shared-memory vector load by shared-window address (volatile: stays
+// between the barriers; no memory clobber: the global stores are not
+// ordered against it)
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(a));
+    return v;
 }
 
 // value readers of gemm_write: the S == 1 tile, and the S > 1 split sum
-// (own tile for s == split, received slices otherwise, in split order)
+// (own tile for s == split, received slices otherwise, in split order);
+// base addresses in the shared window
 template <int kOt>
 struct TileVal {
-    const float *ot;
+    uint32_t ot;
     __device__ __forceinline__ void operator()(int r, int col, float (&v)[8]) const {
-        const float4 *q = reinterpret_cast<const float4 *>(ot + r * kOt + col);
-        const float4 x0 = q[0], x1 = q[1];
+        const uint32_t q = ot + (uint32_t)(r * kOt + col) * 4;
+        const float4 x0 = lds128(q), x1 = lds128(q + 16);
         v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
         v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
     }
@@ -258,16 +290,15 @@ struct TileVal {
 
 template <int kOt>
 struct SplitVal {
-    const float *ot, *rv;
+    uint32_t ot, rv;
     int S, split, r0, nrmax;
     __device__ __forceinline__ void operator()(int r, int col, float (&v)[8]) const {
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = 0.f;
         for (int s0 = 0; s0 < S; ++s0) {  // split order: deterministic
-            const float *src = s0 == split ? ot + (r0 + r) * kOt + col
-                                           : rv + (s0 * nrmax + r) * kOt + col;
-            const float4 x0 = reinterpret_cast<const float4 *>(src)[0];
-            const float4 x1 = reinterpret_cast<const float4 *>(src)[1];
+            const uint32_t q = s0 == split ? ot + (uint32_t)((r0 + r) * kOt + col) * 4
+                                           : rv + (uint32_t)((s0 * nrmax + r) * kOt + col) * 4;
+            const float4 x0 = lds128(q), x1 = lds128(q + 16);
             v[0] += x0.x; v[1] += x0.y; v[2] += x0.z; v[3] += x0.w;
             v[4] += x1.x; v[5] += x1.y; v[6] += x1.z; v[7] += x1.w;
         }
@@ -280,12 +311,16 @@ struct SplitVal {
 template <int G, typename Val>
 __device__ __forceinline__ void gemm_write(const GemmParams &p, int grp, int row0, int nr,
                                            int t, Val val, bool live = true) {
+    unsigned long long *st = p.dbg ? p.dbg + blockIdx.x * 16 : nullptr;
     if (p.epilogue == EPI_SWIGLU)
-        gemm_write_epi<G, EPI_SWIGLU>(p, grp, row0, nr, t, val, live);
+        gemm_write_epi<G, EPI_SWIGLU>(p.out, p.ld_out, p.res, p.ld_res, grp, row0, nr, t, val,
+                                      live, st);
     else if (p.epilogue == EPI_RESIDUAL)
-        gemm_write_epi<G, EPI_RESIDUAL>(p, grp, row0, nr, t, val, live);
+        gemm_write_epi<G, EPI_RESIDUAL>(p.out, p.ld_out, p.res, p.ld_res, grp, row0, nr, t, val,
+                                        live, st);
     else
-        gemm_write_epi<G, EPI_STORE>(p, grp, row0, nr, t, val, live);
+        gemm_write_epi<G, EPI_STORE>(p.out, p.ld_out, p.res, p.ld_res, grp, row0, nr, t, val,
+                                     live, st);
 }
 
 // accumulators -> fp32 tile [64][kOt] in shared memory: thread m owns
@@ -404,8 +439,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const float *dummy = reinterpret_cast<const float *>(smem + kGemmStages * kStageBytes + 128);
     const int nrmax = (p.rows + S - 1) / S;
     const int r0 = split * p.rows / S, r1 = (split + 1) * p.rows / S, nr = r1 - r0;
-    const TileVal<kOt> val_tile{ot};
-    const SplitVal<kOt> val_split{ot, rv, S, split, r0, nrmax};
+    const uint32_t ot_s = smem_u32(ot), rv_s = smem_u32(rv), dummy_s = smem_u32(dummy);
+    const TileVal<kOt> val_tile{ot_s};
+    const SplitVal<kOt> val_split{ot_s, rv_s, S, split, r0, nrmax};
 
     if (warp == 4) {
         // ---------------- TMA producer ----------------
@@ -503,9 +539,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         // instruction warm-up while the main loop streams (no side effects)
         tile_to_smem<G, kOt>(tmem, ot, warp, m, false);
         if (S == 1)
-            gemm_write<G>(p, grp, 0, 1, m, TileVal<kOt>{dummy}, false);
+            gemm_write<G>(p, grp, 0, 1, m, TileVal<kOt>{dummy_s}, false);
         else
-            gemm_write<G>(p, grp, r0, 1, m, SplitVal<kOt>{dummy, dummy, S, -1, 0, 0}, false);
+            gemm_write<G>(p, grp, r0, 1, m, SplitVal<kOt>{dummy_s, dummy_s, S, -1, 0, 0}, false);
         mbar_wait(bar_acc, 0);
         tc_fence_after();
         grid_dependency_wait();  // out / res: after the previous kernel

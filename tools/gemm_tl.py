@@ -35,6 +35,8 @@ for K, Nc in zip(args[0::2], args[1::2]):
                        ("MMA done->partials stored", 2, 3), ("tile stored->cluster barrier", 3, 7),
                        ("MMA issued->acc ready", 2, 8), ("cluster barrier->received", 7, 9),
                        ("received->arrived", 9, 11), ("arrived->reduced", 11, 10),
+                       ("write: enter->1st chunk", 13, 14), ("write: 1st chunk->done", 14, 15),
+                       ("arrived->write enter", 11, 13), ("write done->stamp10", 15, 10),
                        ("reduced->end", 10, 4), ("->CTA end", 3, 4), ("start->end", 0, 4), ("t0->end", None, 4)):
         v = (d[:, b] - (t0 if a is None else d[:, a])) / 1e3
         ok = (d[:, b] > 0) & ((d[:, a] > 0) if a is not None else True)
