@@ -78,6 +78,22 @@ class PackedWeight:
                                   dtype=torch.bfloat16, device=device)
         return self
 
+    @classmethod
+    def empty_layers(cls, L: int, K: int, n: int, device, group: int = 1) -> list:
+        """``L`` uninitialised [K, n] weights carved from ONE allocation (an
+        adoption re-lays out every layer at once; one cudaMalloc, not L)."""
+        if n % (128 * group) or K % 64:
+            raise ValidationError("packed weights need N % 128 == 0 and K % 64 == 0")
+        buf = torch.empty((L, n // (128 * group), K // 64, group, 128, 8, 8),
+                          dtype=torch.bfloat16, device=device)
+        out = []
+        for layer in range(L):
+            self = cls.__new__(cls)
+            self.K, self.N, self.group = K, n, group
+            self.panels = buf[layer]
+            out.append(self)
+        return out
+
     def unpack(self) -> torch.Tensor:
         f, sw = _swizzle_index(self.panels.device)
         b = self.panels[:, :, :, f, sw]                             # the swizzle is an involution

@@ -498,8 +498,8 @@ class HybridDecodeRank:
         packed = self.gemm == "tcgen05"
         if packed:
             from .gemm import PackedWeight
-            wqkv = [PackedWeight.empty(hid, rw, dev) for _ in range(L)]
-            wo = [PackedWeight.empty(S * qpk * hd, hid, dev) for _ in range(L)]
+            wqkv = PackedWeight.empty_layers(L, hid, rw, dev)
+            wo = PackedWeight.empty_layers(L, S * qpk * hd, hid, dev)
         else:
             wqkv = torch.zeros((L, hid, rw), dtype=torch.bfloat16, device=dev)
             wo = torch.zeros((L, S * qpk * hd, hid), dtype=torch.bfloat16, device=dev)
@@ -520,8 +520,8 @@ class HybridDecodeRank:
             shards = sorted(s_ for s_, g in enumerate(shard_owner) if g == self.rank)
             C = len(shards) * (self.model.ffn_intermediate_dim // self.num_shards)
             if packed:
-                w_gu = [PackedWeight.empty(hid, 2 * C, dev) for _ in range(L)]
-                w_d = [PackedWeight.empty(C, hid, dev) for _ in range(L)]
+                w_gu = PackedWeight.empty_layers(L, hid, 2 * C, dev)
+                w_d = PackedWeight.empty_layers(L, C, hid, dev)
             else:
                 w_gu = torch.zeros((L, hid, 2 * C), dtype=torch.bfloat16, device=dev)
                 w_d = torch.zeros((L, C, hid), dtype=torch.bfloat16, device=dev)
