@@ -488,8 +488,29 @@ def mixed_trace(skip=24, n_iter=3, budget=2048, fail=7):
             e_.record()
             torch.cuda.synchronize()
             times.append(s_.elapsed_time(e_))
+        pipe = None
+        if g == alive[0]:
+            # wall clock per iteration with the host plan of iteration k+1
+            # built while the device runs iteration k, against plan-then-serve
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for s, x in zip(steps, xs):
+                eng.serve(eng.plan(s), x)
+                torch.cuda.synchronize()
+            serial = (time.perf_counter() - t0) * 1e3 / len(steps)
+            t0 = time.perf_counter()
+            nxt = eng.plan(steps[0])
+            for k, x in enumerate(xs):
+                cur = nxt
+                eng.serve(cur, x)
+                if k + 1 < len(steps):
+                    nxt = eng.plan(steps[k + 1])
+                torch.cuda.synchronize()
+            piped = (time.perf_counter() - t0) * 1e3 / len(steps)
+            pipe = {"serial_wall_ms": round(serial, 3), "pipelined_wall_ms": round(piped, 3)}
         per_rank.append({"rank": g, "iter_ms": [round(t, 3) for t in times],
                          "host_plan_ms": round(plan_ms, 2),
+                         **({"host_overlap": pipe} if pipe else {}),
                          "kv_read_gb": [round(p.kv_read_bytes / 1e9, 3) for p in plans],
                          "prefill_attn_tflop": [round(p.attn_flops / 1e12, 3) for p in plans],
                          "launches": [eng.serve_launches(p) for p in plans]})
