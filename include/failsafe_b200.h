@@ -159,6 +159,13 @@ typedef struct fs_decode_desc {
     int32_t device;            /* CUDA device ordinal the launch runs on    */
     int32_t config;            /* 0 = default kernel configuration          */
     int32_t flags;             /* FS_DECODE_* bits                          */
+    /* static partition skew (0 / 0 = even): the first head_ctas CTAs --
+     * dispatched first, onto the SMs the preceding launch leaves free, so
+     * they stage their first pages early -- each take head_pages more pages
+     * than the others.  Deterministic: the partition depends only on these
+     * fields and the page count (decode_cta configurations). */
+    int32_t head_ctas;
+    int32_t head_pages;
 } fs_decode_desc;
 
 /* fs_decode_desc.flags: the caller guarantees that the kernel launched
@@ -340,6 +347,11 @@ int fs_gemm_skinny(const void *x, int64_t ld_x, int32_t rows, int32_t K, const v
                    int64_t ld_w, int32_t w_layout, int32_t N, void *out, int64_t ld_out, const void *res,
                    int64_t ld_res, int32_t epilogue, float *workspace, int64_t ws_floats,
                    int32_t *sems, int32_t device, void *stream);
+
+/* k-split count (CTAs per column group; grid = N / 128 / G x splits) that
+ * fs_gemm_skinny uses for this shape and W layout on `device` (>= 1), or a
+ * negative status. */
+int fs_gemm_plan(int32_t device, int32_t K, int32_t N, int32_t w_layout);
 
 /* TP MLP partial nonlinearity: out[r, c] = silu(h[r, c]) * h[r, cols + c]
  * (bf16; h row stride ld >= 2*cols; gated FFN of core.py:93-95). */

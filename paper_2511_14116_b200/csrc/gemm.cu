@@ -703,6 +703,39 @@ extern "C" int64_t fs_gemm_workspace_floats(int device, int32_t N, int32_t epilo
     return 1;
 }
 
+static int gemm_plan_status(int32_t device, int32_t K, int32_t N, int32_t w_layout, int *splits) {
+    FS_CHECK_ARG(K > 0 && K % kStepK == 0 && N > 0 && N % kTileM == 0 && w_layout >= 0 &&
+                     w_layout <= 2, "bad GEMM shape");
+    const int sms = sm_count(device);
+    if (sms <= 0) return fail(FS_ECUDA, "cannot query SM count");
+    const int group = w_layout == 2 ? 2 : 1;
+    FS_CHECK_ARG((N / kTileM) % group == 0, "W layout 2 needs an even number of tiles");
+    int cur = 0;
+    FS_CUDA(cudaGetDevice(&cur));
+    FS_CUDA(cudaSetDevice(device));
+    const size_t smem = gemm_smem();
+    FS_CUDA(cudaFuncSetAttribute(gemm_skinny_kernel<1, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FS_CUDA(cudaFuncSetAttribute(gemm_skinny_kernel<1, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FS_CUDA(cudaFuncSetAttribute(gemm_skinny_kernel<2, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int groups = N / kTileM / group, nk = K / kStepK;
+    *splits = w_layout == 0 ? gemm_splits<1, false>(device, sms, groups, nk)
+              : group == 1  ? gemm_splits<1, true>(device, sms, groups, nk)
+                            : gemm_splits<2, true>(device, sms, groups, nk);
+    FS_CUDA(cudaSetDevice(cur));
+    return FS_OK;
+}
+
+// k-split count (= CTAs per column group) of a launch of this shape, or
+// -status
+extern "C" int fs_gemm_plan(int32_t device, int32_t K, int32_t N, int32_t w_layout) {
+    int s = 0;
+    const int rc = gemm_plan_status(device, K, N, w_layout, &s);
+    return rc == FS_OK ? s : -rc;
+}
+
 extern "C" int fs_gemm_skinny(const void *x, int64_t ld_x, int32_t rows, int32_t K, const void *w,
                               int64_t ld_w, int32_t w_layout, int32_t N, void *out, int64_t ld_out,
                               const void *res, int64_t ld_res, int32_t epilogue, float *workspace,
