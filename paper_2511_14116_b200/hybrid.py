@@ -27,7 +27,6 @@ global model, so the sum over ranks reproduces the single-GPU result.
 
 from __future__ import annotations
 
-
 import math
 
 import numpy as np
