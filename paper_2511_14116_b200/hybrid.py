@@ -570,6 +570,8 @@ class HybridDecodeRank:
             self.act = torch.empty((self.batch, C), dtype=torch.bfloat16, device=dev)
         self.qkv = torch.empty((self.batch, rw), dtype=torch.bfloat16, device=dev)
         self.o = torch.zeros((self.batch * S, qpk, hd), dtype=torch.bfloat16, device=dev)
+        if packed:
+            self._skew_decode()  # the QKV grid changed with the slots
         self._graph = None
         return fresh
 
