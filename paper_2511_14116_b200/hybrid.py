@@ -113,6 +113,11 @@ class HybridDecodeRank:
     (None = no exchange: world 1 or single-GPU emulation).
     """
 
+    # K1 partition skew toward the CTAs that start during the QKV GEMM
+    # (fs_decode_desc.head_pages).  Off: measured +0.8% on the C3 N=8 rank
+    # step at 16 pages but -4% at N=7 and slower attention-only graphs.
+    K1_HEAD_PAGES = 0
+
     def __init__(self, model: ModelSpec, owner, rank: int, routing, batch: int, capacity: int,
                  device=None, seed: int = 0, group=None, page_order: str = "contiguous",
                  config: int = 0, mlp: bool = False, shard_owner=None, gemm: str = "tcgen05",
@@ -222,8 +227,7 @@ class HybridDecodeRank:
         sms = torch.cuda.get_device_properties(self.device).multi_processor_count
         grid = (self.p_qkv[0].N // 128 // self.p_qkv[0].group) * max(plan, 1)
         self.cache.head_ctas = max(0, sms - grid)
-        # ~ the pages they stage early (C3 N=8 rank step 6.35 -> 6.29 ms)
-        self.cache.head_pages = 16
+        self.cache.head_pages = self.K1_HEAD_PAGES
 
     # ------------------------------------------------------------------ api --
     def set_lengths(self, lens) -> None:
