@@ -159,13 +159,6 @@ typedef struct fs_decode_desc {
     int32_t device;            /* CUDA device ordinal the launch runs on    */
     int32_t config;            /* 0 = default kernel configuration          */
     int32_t flags;             /* FS_DECODE_* bits                          */
-    /* static partition skew (0 / 0 = even): the first head_ctas CTAs --
-     * dispatched first, onto the SMs the preceding launch leaves free, so
-     * they stage their first pages early -- each take head_pages more pages
-     * than the others.  Deterministic: the partition depends only on these
-     * fields and the page count (decode_cta configurations). */
-    int32_t head_ctas;
-    int32_t head_pages;
 } fs_decode_desc;
 
 /* fs_decode_desc.flags: the caller guarantees that the kernel launched

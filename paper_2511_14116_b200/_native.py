@@ -39,8 +39,7 @@ class DecodeDesc(C.Structure):
         ("item_sem", C.c_void_p), ("n_items", C.c_int32), ("q_per_kv", C.c_int32), ("scale", C.c_float),
         ("out_fp32", C.c_int32), ("out", C.c_void_p), ("part_o", C.c_void_p),
         ("part_lse", C.c_void_p), ("partial_slots", C.c_int64), ("device", C.c_int32),
-        ("config", C.c_int32), ("flags", C.c_int32), ("head_ctas", C.c_int32),
-        ("head_pages", C.c_int32),
+        ("config", C.c_int32), ("flags", C.c_int32),
     ]
 
 

@@ -51,36 +51,6 @@ struct DecodeParams {
     int64_t n_warps;  // W of the stream-K partition
     int32_t tab_cache;  // decode_cta_kernel: page_off / item_seq staged in smem (n_items <= kTabItems)
     int32_t early;      // FS_DECODE_EARLY_PREFETCH: tables + first pages read before griddepcontrol.wait
-    int32_t head_ctas, head_pages;  // partition skew (decode_cta_kernel)
-};
-
-// decode_cta_kernel's static partition of P pages over C CTAs: an even
-// split of P - E*D, the first E CTAs D pages more (E = head_ctas, D =
-// head_pages, D clamped so every share stays >= 0); E = D = 0 is c*P/C
-struct CtaPart {
-    int64_t P, C, E, D, Pp;
-    __device__ __forceinline__ CtaPart(int64_t P_, int64_t C_, int E_, int D_)
-        : P(P_), C(C_), E(E_ < C_ ? E_ : C_), D(D_) {
-        if (E <= 0 || D <= 0 || P < E * D) {
-            E = 0;
-            D = 0;
-        }
-        Pp = P - E * D;
-    }
-    __device__ __forceinline__ int64_t start(int64_t c) const {
-        return c * Pp / C + (c < E ? c : E) * D;
-    }
-    // the CTA whose range holds page x (largest c with start(c) <= x)
-    __device__ __forceinline__ int64_t owner(int64_t x) const {
-        int64_t lo = 0, hi = C - 1;
-        while (lo < hi) {
-            const int64_t mid = (lo + hi + 1) >> 1;
-            if (start(mid) <= x) lo = mid; else hi = mid - 1;
-        }
-        return lo;
-    }
-    __device__ __forceinline__ bool live(int64_t c) const { return start(c) < start(c + 1); }
-    __device__ __forceinline__ bool all_live() const { return Pp >= C; }
 };
 
 // items whose page offsets and block-table rows decode_cta_kernel stages in
@@ -648,9 +618,6 @@ extern "C" int fs_decode_attention(const fs_decode_desc *d, void *stream) {
     prm.part_lse = d->part_lse;
     prm.n_warps = W;
     prm.early = (d->flags & FS_DECODE_EARLY_PREFETCH) ? 1 : 0;
-    FS_CHECK_ARG(d->head_ctas >= 0 && d->head_pages >= 0, "negative partition skew");
-    prm.head_ctas = d->head_ctas;
-    prm.head_pages = d->head_pages;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (d->config) {
 #define FS_CFG_CASE(i, w, s, c, k) \

@@ -47,8 +47,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_cta_kernel(const DecodeP
     const int64_t P = off[p.n_items];
     const int64_t C = p.n_warps;  // partition units = CTAs
     const int64_t c = blockIdx.x;
-    const CtaPart part(P, C, p.head_ctas, p.head_pages);
-    const int64_t x0 = part.start(c), x1 = part.start(c + 1);
+    const int64_t x0 = c * P / C, x1 = (c + 1) * P / C;
     grid_launch_dependents();  // the next launch may stage its pages early
     if (x0 >= x1) return;  // CTA-uniform
 
@@ -295,11 +294,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_cta_kernel(const DecodeP
             named_bar(1, NT);
             if (threadIdx.x == 0) s_prev = atomicAdd(p.item_sem + item, 1);
             named_bar(1, NT);
-            const int64_t clo = part.owner(ib), chi = part.owner(ie - 1);
+            const int64_t clo = owner_warp(ib, C, P), chi = owner_warp(ie - 1, C, P);
             int nseg = (int)(chi - clo + 1);
-            if (!part.all_live()) {
+            if (P < C) {
                 nseg = 0;
-                for (int64_t s = clo; s <= chi; ++s) nseg += part.live(s);
+                for (int64_t s = clo; s <= chi; ++s) nseg += warp_live(s, C, P);
             }
             if (s_prev == nseg - 1) {
                 // last CTA of the item: merge its (up to ~all-CTA) partials.
@@ -309,7 +308,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_cta_kernel(const DecodeP
                 // trip for the usual <= WARPS segments -- then the warps'
                 // states are combined in smem.
                 __threadfence();
-                const bool all_live = part.all_live();
+                const bool all_live = P >= C;
                 const int qpk = p.qpk;
                 float mw[FS_MAX_Q_PER_KV], lw[FS_MAX_Q_PER_KV];
                 float4 acc[FS_MAX_Q_PER_KV];
@@ -320,7 +319,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_cta_kernel(const DecodeP
                     acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
                 }
                 for (int64_t s = clo + warp; s <= chi; s += WARPS) {
-                    if (!all_live && !part.live(s)) continue;
+                    if (!all_live && !warp_live(s, C, P)) continue;
                     const float *ls = p.part_lse + (item + s) * qpk;
                     const float4 *os = reinterpret_cast<const float4 *>(p.part_o + (item + s) * qpk * kHeadDim);
                     float lv[FS_MAX_Q_PER_KV];

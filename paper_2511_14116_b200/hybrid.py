@@ -113,11 +113,6 @@ class HybridDecodeRank:
     (None = no exchange: world 1 or single-GPU emulation).
     """
 
-    # K1 partition skew toward the CTAs that start during the QKV GEMM
-    # (fs_decode_desc.head_pages).  Off: measured +0.8% on the C3 N=8 rank
-    # step at 16 pages but -4% at N=7 and slower attention-only graphs.
-    K1_HEAD_PAGES = 0
-
     def __init__(self, model: ModelSpec, owner, rank: int, routing, batch: int, capacity: int,
                  device=None, seed: int = 0, group=None, page_order: str = "contiguous",
                  config: int = 0, mlp: bool = False, shard_owner=None, gemm: str = "tcgen05",
@@ -216,18 +211,6 @@ class HybridDecodeRank:
         del self.wqkv, self.wo
         torch.cuda.empty_cache()
         self.skinny = SkinnyGemm(widest, self.device)
-        self._skew_decode()
-
-    def _skew_decode(self) -> None:
-        """K1 follows the QKV GEMM: its first CTAs land on the SMs the GEMM
-        grid leaves free, stage their first pages while the GEMM runs and so
-        start ahead -- give those CTAs a larger static share."""
-        plan = N.lib.fs_gemm_plan(self.skinny.index, self.p_qkv[0].K, self.p_qkv[0].N,
-                                  self.p_qkv[0].group)
-        sms = torch.cuda.get_device_properties(self.device).multi_processor_count
-        grid = (self.p_qkv[0].N // 128 // self.p_qkv[0].group) * max(plan, 1)
-        self.cache.head_ctas = max(0, sms - grid)
-        self.cache.head_pages = self.K1_HEAD_PAGES
 
     # ------------------------------------------------------------------ api --
     def set_lengths(self, lens) -> None:
@@ -574,8 +557,6 @@ class HybridDecodeRank:
             self.act = torch.empty((self.batch, C), dtype=torch.bfloat16, device=dev)
         self.qkv = torch.empty((self.batch, rw), dtype=torch.bfloat16, device=dev)
         self.o = torch.zeros((self.batch * S, qpk, hd), dtype=torch.bfloat16, device=dev)
-        if packed:
-            self._skew_decode()  # the QKV grid changed with the slots
         self._graph = None
         return fresh
 

@@ -167,8 +167,6 @@ class PagedKVCache:
         # in HybridDecodeRank); otherwise (K3 / K4 / restores just before) the
         # launch reads nothing before its PDL wait
         self.early_prefetch = False
-        # static partition skew for CTAs that start early (fs_decode_desc)
-        self.head_ctas, self.head_pages = 0, 0
         self.fused = None  # (qoff, koff, voff) of the fused-qkv layout
         self._install(work, bt.astype(np.int32))
 
@@ -316,7 +314,7 @@ class PagedKVCache:
     # -------------------------------------------------------------- decode --
     def _desc(self, layer, q, out, qkv, scale):
         key = (layer, q.data_ptr(), out.data_ptr(), out.dtype, qkv, scale, self.config,
-               self.early_prefetch, self.head_ctas, self.head_pages)
+               self.early_prefetch)
         d = self._descs.get(key)
         if d is not None:
             return d
@@ -351,7 +349,6 @@ class PagedKVCache:
         d.device = self.dev_index
         d.config = self.config
         d.flags = N.DECODE_EARLY_PREFETCH if self.early_prefetch else 0
-        d.head_ctas, d.head_pages = self.head_ctas, self.head_pages
         self._descs[key] = d
         return d
 

@@ -105,46 +105,6 @@ def test_decode_hybrid_rank_ragged(qpk, config):
             _close(out.cpu().numpy(), exp)
 
 
-@pytest.mark.parametrize("skew", [(68, 16), (148, 3), (5, 4000), (1, 1)])
-def test_decode_partition_skew(skew):
-    """fs_decode_desc.head_ctas / head_pages (the first CTAs take a larger
-    static share): same results as the oracle for ragged items, including a
-    skew larger than the page count (clamped to the even split) and one that
-    leaves most CTAs without pages; repeated launches are bit-identical."""
-    from oracle.placement import owner_table
-    owner = owner_table("hybrid", 2, 8, range(7))
-    lens = [1, 15, 16, 17, 33, 300, 1000, 4097, 2, 2048, 511]
-    routing = {r: r % 7 for r in range(len(lens))}
-    from oracle.attention import head_decode
-    qpk = 8
-    gen = torch.Generator().manual_seed(sum(skew))
-    work, cache = _build(owner, 0, routing, lens, qpk)
-    cache.head_ctas, cache.head_pages = skew
-    kv = _fill(cache, work, lens, gen)
-    n_rows = len(lens) * work.n_slots
-    q = _bf16(torch.randn((n_rows, qpk, 128), generator=gen))
-    qn = q.double().numpy()
-    out = torch.zeros((n_rows, qpk, 128), dtype=torch.float32, device="cuda")
-    q_dev = q.cuda()
-    for layer in range(2):
-        out.zero_()
-        cache.decode_layer(layer, q_dev, out)
-        torch.cuda.synchronize()
-        first = out.clone()
-        cache.decode_layer(layer, q_dev, out)
-        torch.cuda.synchronize()
-        assert torch.equal(first, out)
-        a, b = work.seg_items[layer], work.seg_items[layer + 1]
-        exp = np.zeros((n_rows, qpk, 128))
-        for i in range(a, b):
-            r, j = work.item_req[i], work.item_slot[i]
-            row = r * work.n_slots + j
-            k, v = kv[i]
-            exp[row] = head_decode(qn[row], k[:lens[r]], v[:lens[r]], 1 / math.sqrt(128))
-        _close(out.cpu().numpy(), exp)
-    assert int(cache.item_sem.abs().sum()) == 0
-
-
 def test_decode_bf16_output_and_determinism():
     from oracle.placement import owner_table
     owner = owner_table("cyclic", 1, 8, range(2))

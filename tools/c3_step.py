@@ -16,7 +16,6 @@ ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--time", action="store_true", help="graph-time the step instead")
 ap.add_argument("--model", default="70b")
 ap.add_argument("--config", type=int, default=0, help="K1 kernel config")
-ap.add_argument("--head-pages", type=int, default=None, help="K1 partition skew override")
 a = ap.parse_args()
 model = bench.llama70b() if a.model == "70b" else bench.llama8b()
 base = 8 if a.model == "70b" else a.world
@@ -28,13 +27,10 @@ for f in (7, 3, 5)[:base - a.world]:
 routing = bench.route(64, alive, 4096)
 bench.GEMM_BACKEND = a.gemm
 eng = bench.build_rank(model, plan, a.rank, routing, 64, 4096, None, a.config)
-if a.head_pages is not None:
-    eng.cache.head_pages = a.head_pages
-    eng._graph = None
 if a.time:
     ms = bench.time_graph(eng.step, 10, 3)
     wb, kb = eng.weight_bytes(), bench.step_kv_bytes(eng)
-    print(f"{a.model} world {a.world} rank {a.rank} {a.gemm} K1 config {a.config} skew {eng.cache.head_ctas}x{eng.cache.head_pages}: step {ms:.3f} ms, weights {wb/1e9:.2f} GB "
+    print(f"{a.model} world {a.world} rank {a.rank} {a.gemm} K1 config {a.config}: step {ms:.3f} ms, weights {wb/1e9:.2f} GB "
           f"kv {kb/1e9:.2f} GB, {(wb+kb)/ms/1e6:.0f} GB/s")
 else:
     for _ in range(a.steps):

@@ -15,7 +15,6 @@ TESTS=(
   "tests/test_recovery_gpu.py::test_backup_then_restore_is_bitexact"
   "tests/test_recovery_gpu.py::test_restore_failed_rank_onto_survivor_per_plan"
   "tests/test_gemm_gpu.py::test_store"
-  "tests/test_decode_gpu.py::test_decode_partition_skew"
   "tests/test_gemm_gpu.py::test_split_reduction_rows"
   "tests/test_gemm_gpu.py::test_packed_panels_match_row_major"
   "tests/test_exchange_gpu.py::test_fused_exchange_decode_step_matches_emulation"
