@@ -126,3 +126,37 @@ def test_split_reduction_rows(rows):
     torch.cuda.synchronize()
     _close(out, base.float() + _ref(x, w))
     assert int(gemm.sems.abs().sum()) == 0
+
+
+# the decode-step projections at the BASELINE shapes (per rank): C2 (8B,
+# world 1) and C3 (70B, hybrid(8) and the 5-survivor on-demand target),
+# packed weights and the production epilogues
+_CONFIG_SHAPES = {
+    "c2": [(4096, 6144, 0), (4096, 4096, 1), (4096, 2 * 14336, 2), (14336, 4096, 1)],
+    "c3_n8": [(8192, 1280, 0), (1024, 8192, 0), (8192, 2 * 3584, 2), (3584, 8192, 0)],
+    "c3_n5": [(8192, 5120, 0), (4096, 8192, 0), (8192, 2 * 5760, 2), (5760, 8192, 0)],
+}
+
+
+@pytest.mark.parametrize("config", sorted(_CONFIG_SHAPES))
+def test_projections_at_baseline_shapes(config):
+    from paper_2511_14116_b200.gemm import PackedWeight, SkinnyGemm, interleave_gate_up
+    gemm = SkinnyGemm()
+    g = torch.Generator(device="cuda").manual_seed(len(config))
+    for K, N, epi in _CONFIG_SHAPES[config]:
+        x = torch.randn((64, K), device="cuda", generator=g).to(torch.bfloat16)
+        w = (torch.randn((K, N), device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+        if epi == 2:
+            w = interleave_gate_up(w[:, :N // 2], w[:, N // 2:])
+        n_out = N // 2 if epi == 2 else N
+        base = torch.randn((64, n_out), device="cuda", generator=g).to(torch.bfloat16)
+        out = base.clone()
+        gemm(x, PackedWeight(w), out, epi)
+        torch.cuda.synchronize()
+        ref = _ref(x, w)
+        if epi == 2:
+            blk = ref.view(64, -1, 2, 64)
+            ref = torch.nn.functional.silu(blk[:, :, 0].reshape(64, -1)) * blk[:, :, 1].reshape(64, -1)
+        elif epi == 1:
+            ref = ref + base.float()
+        _close(out, ref)
