@@ -77,6 +77,11 @@ __device__ __forceinline__ uint32_t *flags_of(uint8_t *buf, int64_t data_bytes) 
 
 __global__ void __launch_bounds__(256) ar_residual_kernel(const ArParams p) {
     __shared__ uint32_t s_use;
+    // programmatic dependent launch: the next projection's CTAs may start
+    // staging their weights while this exchange waits for the peers; this
+    // kernel's own reads (the partial, x) wait for the producing GEMM
+    grid_launch_dependents();
+    grid_dependency_wait();
     uint32_t *mine = flags_of(p.peer[p.rank], p.data_bytes);
     uint32_t *use_ctr = mine + FS_AR_MAX_WORLD, *done_ctr = use_ctr + 1;
     if (threadIdx.x == 0) s_use = *reinterpret_cast<volatile uint32_t *>(use_ctr) + 1u;
@@ -161,6 +166,8 @@ __device__ __forceinline__ void spin_flags(const uint32_t *f, int world, uint32_
 // caps the grid well below one CTA per SM.
 __global__ void __launch_bounds__(256) ar_residual_2shot_kernel(const ArParams p) {
     __shared__ uint32_t s_use;
+    grid_launch_dependents();  // as ar_residual_kernel
+    grid_dependency_wait();
     uint32_t *mine = flags_of(p.peer[p.rank], p.data_bytes);
     uint32_t *use_ctr = mine + FS_AR_MAX_WORLD, *done_ctr = use_ctr + 1, *done1 = mine + kDone1;
     if (threadIdx.x == 0) s_use = *reinterpret_cast<volatile uint32_t *>(use_ctr) + 1u;
@@ -314,19 +321,32 @@ extern "C" int fs_ar_residual_mode(void *const *peers, int32_t rank, int32_t wor
     prm.x = static_cast<__nv_bfloat16 *>(x);
     if (mode == 0) mode = (world > 2 && n * 2 >= two_shot_min_bytes()) ? 2 : 1;
     const int64_t need = (n / 8 + 255) / 256;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // launched with PDL: 256 threads and no shared memory, so the grid is
+    // resident next to a projection GEMM's CTAs (one per SM): neither the
+    // early start nor the two-shot form's all-CTAs-resident wait can be
+    // starved by the dependent launch
+    cudaLaunchConfig_t lc = {};
+    lc.blockDim = dim3(256);
+    lc.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
     if (mode == 2) {
         // every CTA resident at once (phase 2 waits on phase 1 of the grid)
         int grid = ctas > 0 ? ctas : 64;
         if (grid > 64) grid = 64;
         if (grid > need) grid = (int)(need > 0 ? need : 1);
-        ar_residual_2shot_kernel<<<grid, 256, 0, st>>>(prm);
-        return cuda_status(cudaGetLastError(), "ar_residual_2shot_kernel launch");
+        lc.gridDim = dim3(grid);
+        FS_CUDA(cudaLaunchKernelEx(&lc, ar_residual_2shot_kernel, prm));
+        return FS_OK;
     }
     int grid = ctas > 0 ? ctas : 148;
     if (grid > need) grid = (int)(need > 0 ? need : 1);
-    ar_residual_kernel<<<grid, 256, 0, st>>>(prm);
-    return cuda_status(cudaGetLastError(), "ar_residual_kernel launch");
+    lc.gridDim = dim3(grid);
+    FS_CUDA(cudaLaunchKernelEx(&lc, ar_residual_kernel, prm));
+    return FS_OK;
 }
 
 extern "C" int fs_ar_residual(void *const *peers, int32_t rank, int32_t world, int64_t n,
