@@ -710,17 +710,22 @@ static int gemm_plan_status(int32_t device, int32_t K, int32_t N, int32_t w_layo
     FS_CUDA(cudaGetDevice(&cur));
     FS_CUDA(cudaSetDevice(device));
     const size_t smem = gemm_smem();
-    FS_CUDA(cudaFuncSetAttribute(gemm_skinny_kernel<1, false>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    FS_CUDA(cudaFuncSetAttribute(gemm_skinny_kernel<1, true>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    FS_CUDA(cudaFuncSetAttribute(gemm_skinny_kernel<2, true>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int groups = N / kTileM / group, nk = K / kStepK;
-    *splits = w_layout == 0 ? gemm_splits<1, false>(device, sms, groups, nk)
-              : group == 1  ? gemm_splits<1, true>(device, sms, groups, nk)
-                            : gemm_splits<2, true>(device, sms, groups, nk);
-    FS_CUDA(cudaSetDevice(cur));
+    cudaError_t e = cudaFuncSetAttribute(gemm_skinny_kernel<1, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(gemm_skinny_kernel<1, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(gemm_skinny_kernel<2, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) {
+        const int groups = N / kTileM / group, nk = K / kStepK;
+        *splits = w_layout == 0 ? gemm_splits<1, false>(device, sms, groups, nk)
+                  : group == 1  ? gemm_splits<1, true>(device, sms, groups, nk)
+                                : gemm_splits<2, true>(device, sms, groups, nk);
+    }
+    cudaSetDevice(cur);  // restored on every path
+    FS_CUDA(e);
     return FS_OK;
 }
 
