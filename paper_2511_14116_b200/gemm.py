@@ -56,7 +56,7 @@ class PackedWeight:
             raise ValidationError("packed weights need N % 128 == 0 and K % 64 == 0")
         tiles = n // 128
         if group is None:
-            group = 2 if tiles > _sm_count(w.device) and tiles % 2 == 0 else 1
+            group = auto_group(w.device, tiles)
         if group not in (1, 2) or tiles % group:
             raise ValidationError(f"bad column group {group} for {tiles} tiles")
         self.K, self.N, self.group = K, n, group
@@ -79,9 +79,12 @@ class PackedWeight:
         return self
 
     @classmethod
-    def empty_layers(cls, L: int, K: int, n: int, device, group: int = 1) -> list:
+    def empty_layers(cls, L: int, K: int, n: int, device, group: int = None) -> list:
         """``L`` uninitialised [K, n] weights carved from ONE allocation (an
-        adoption re-lays out every layer at once; one cudaMalloc, not L)."""
+        adoption re-lays out every layer at once; one cudaMalloc, not L);
+        ``group`` None: the layout packing would pick."""
+        if group is None:
+            group = auto_group(device, n // 128)
         if n % (128 * group) or K % 64:
             raise ValidationError("packed weights need N % 128 == 0 and K % 64 == 0")
         buf = torch.empty((L, n // (128 * group), K // 64, group, 128, 8, 8),
@@ -98,6 +101,12 @@ class PackedWeight:
         f, sw = _swizzle_index(self.panels.device)
         b = self.panels[:, :, :, f, sw]                             # the swizzle is an involution
         return b.permute(1, 4, 5, 0, 2, 3).reshape(self.K, self.N)
+
+
+def auto_group(device, tiles: int) -> int:
+    """Tiles per CTA of a packed weight: two when the 128-column tiles
+    outnumber the SMs (and pair up), else one."""
+    return 2 if tiles > _sm_count(device) and tiles % 2 == 0 else 1
 
 
 def _swizzle_index(device):

@@ -362,8 +362,7 @@ class HybridDecodeRank:
                 (base + (qw + (S + j) * hd) * 2, rw * 2, hd * 2, hid, qb + kb),   # Wv
                 (o_addr, qpk * hd * hid * 2, qpk * hd * hid * 2, 1, qb + 2 * kb)]  # Wo
 
-    # packed weights (gemm.PackedWeight, one column group): 16 KB blocks,
-    # a 128-column tile's blocks contiguous over k.  A head piece is [Wq
+    # packed weights (gemm.PackedWeight): 16 KB blocks.  A head piece is [Wq
     # panels (qpk tiles) | Wk panel | Wv panel | Wo: per output tile, the
     # head's 2 qpk k-step blocks]; a shard piece is [gate/up panels (w/64
     # interleaved tiles) | Wd: per output tile, the shard's w/64 k-step
@@ -371,35 +370,44 @@ class HybridDecodeRank:
     # GEMM streams, so adoption is plain block copies.
     _BLK = 16384
 
+    @classmethod
+    def _blocks(cls, pw, t0: int, nt: int, s0: int, ns: int, off: int) -> list:
+        """Blocks (t, s), t in [t0, t0+nt), s in [s0, s0+ns), of a packed
+        weight as parts of a piece in the canonical [t][s] order (the
+        one-tile layout's) from piece offset ``off``.  One-tile groups: one
+        (2-D) run; two-tile groups interleave the pair's blocks per step,
+        so each tile is a strided run of its own."""
+        B, nk, base = cls._BLK, pw.K // 64, pw.panels.data_ptr()
+        if pw.group == 1:
+            if ns == nk:
+                return [(base + t0 * nk * B, nt * nk * B, nt * nk * B, 1, off)]
+            return [(base + (t0 * nk + s0) * B, nk * B, ns * B, nt, off)]
+        return [(base + (((t // 2) * nk + s0) * 2 + t % 2) * B, 2 * B, B, ns, off + i * ns * B)
+                for i, t in enumerate(range(t0, t0 + nt))]
+
     def _head_parts_packed(self, layer: int, j: int, p_qkv=None, p_o=None, S=None):
         p_qkv = self.p_qkv if p_qkv is None else p_qkv
         p_o = self.p_o if p_o is None else p_o
         S = self.n_slots if S is None else S
         qpk, hid, B = self.qpk, self.model.hidden_dim, self._BLK
         q, o = p_qkv[layer], p_o[layer]
-        if q.group != 1 or o.group != 1:
-            raise ValidationError("failover needs one-tile column groups")
-        panel = (hid // 64) * B
-        qb, base = qpk * panel, q.panels.data_ptr()
-        nk_o = o.K // 64
-        return [(base + j * qb, qb, qb, 1, 0),                                  # Wq
-                (base + (S * qpk + j) * panel, panel, panel, 1, qb),             # Wk
-                (base + (S * qpk + S + j) * panel, panel, panel, 1, qb + panel),  # Wv
-                (o.panels.data_ptr() + j * 2 * qpk * B, nk_o * B, 2 * qpk * B, hid // 128,
-                 qb + 2 * panel)]                                                # Wo
+        nk = hid // 64
+        panel = nk * B
+        qb = qpk * panel
+        return (self._blocks(q, j * qpk, qpk, 0, nk, 0) +                         # Wq
+                self._blocks(q, S * qpk + j, 1, 0, nk, qb) +                      # Wk
+                self._blocks(q, S * qpk + S + j, 1, 0, nk, qb + panel) +          # Wv
+                self._blocks(o, 0, hid // 128, j * 2 * qpk, 2 * qpk, qb + 2 * panel))  # Wo
 
     def _shard_parts_packed(self, layer: int, k: int, p_gu=None, p_d=None):
         p_gu = self.p_gu if p_gu is None else p_gu
         p_d = self.p_d if p_d is None else p_d
         hid, B = self.model.hidden_dim, self._BLK
         gu, d = p_gu[layer], p_d[layer]
-        if gu.group != 1 or d.group != 1:
-            raise ValidationError("failover needs one-tile column groups")
         tw = (self.model.ffn_intermediate_dim // self.num_shards) // 64
-        panel = (hid // 64) * B
-        return [(gu.panels.data_ptr() + k * tw * panel, tw * panel, tw * panel, 1, 0),  # Wg|Wu
-                (d.panels.data_ptr() + k * tw * B, (d.K // 64) * B, tw * B, hid // 128,
-                 tw * panel)]                                                     # Wd
+        nk = hid // 64
+        return (self._blocks(gu, k * tw, tw, 0, nk, 0) +                          # Wg|Wu
+                self._blocks(d, 0, hid // 128, k * tw, tw, tw * nk * B))            # Wd
 
     def _shard_parts(self, layer: int, k: int, w_gu=None, w_d=None):
         """Local FFN shard ``k`` of ``layer`` as the parts of a canonical

@@ -160,3 +160,37 @@ def test_projections_at_baseline_shapes(config):
         elif epi == 1:
             ref = ref + base.float()
         _close(out, ref)
+
+
+@pytest.mark.parametrize("t0,nt,s0,ns", [(0, 1, 0, 16), (3, 5, 0, 16), (2, 4, 5, 7), (0, 160, 3, 2)])
+def test_packed_pieces_are_canonical_across_column_groups(t0, nt, s0, ns):
+    """Failover pieces of packed weights (HybridDecodeRank._blocks): the
+    two-tile layout yields the same piece bytes as the one-tile layout
+    (the canonical [tile][step] order), and writing a piece back into a
+    two-tile weight restores its blocks."""
+    from paper_2511_14116_b200.gemm import PackedWeight
+    from paper_2511_14116_b200.hostmirror import SegmentCopy
+    from paper_2511_14116_b200.hybrid import HybridDecodeRank as H
+    g = torch.Generator(device="cuda").manual_seed(t0 + nt + s0 + ns)
+    w = torch.randn((1024, 160 * 128), device="cuda", generator=g).to(torch.bfloat16)
+    p1, p2 = PackedWeight(w, 1), PackedWeight(w, 2)
+    nbytes = nt * ns * 16384
+    pieces = []
+    for pw in (p1, p2):
+        buf = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+        seg = SegmentCopy()
+        H._to_piece(seg, H._blocks(pw, t0, nt, s0, ns, 0), buf.data_ptr())
+        seg.run(buf.device)
+        pieces.append(buf)
+    torch.cuda.synchronize()
+    assert torch.equal(pieces[0], pieces[1])
+    back = PackedWeight.empty(1024, 160 * 128, "cuda", group=2)
+    back.panels.copy_(p2.panels)
+    for t in range(t0, t0 + nt):  # clobber the target blocks first
+        for s in range(s0, s0 + ns):
+            back.panels[t // 2, s, t % 2].zero_()
+    seg = SegmentCopy()
+    H._from_piece(seg, H._blocks(back, t0, nt, s0, ns, 0), pieces[0].data_ptr())
+    seg.run(back.panels.device)
+    torch.cuda.synchronize()
+    assert torch.equal(back.panels, p2.panels)
