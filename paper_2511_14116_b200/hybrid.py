@@ -618,6 +618,24 @@ class HybridDecodeRank:
             self._layers()
         self._graph = g
 
+    def step_io(self, x_host: torch.Tensor, y_host: torch.Tensor) -> torch.Tensor:
+        """One decode step from pinned host ``x_host`` into pinned host
+        ``y_host``: the input copy, every layer and the result copy are ONE
+        CUDA-graph launch (captured on first use for this pair of buffers);
+        the caller synchronizes before reading ``y_host``."""
+        io = getattr(self, "_io", None)
+        if io is None or io[1] is not x_host or io[2] is not y_host or self._graph is None:
+            if self._graph is None:
+                self.capture()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.x.copy_(x_host, non_blocking=True)
+                self._layers()
+                y_host.copy_(self.x, non_blocking=True)
+            self._io = io = (g, x_host, y_host)
+        io[0].replay()
+        return y_host
+
     def step(self, x: torch.Tensor = None) -> torch.Tensor:
         """One decode step: x [B, hidden] bf16 (device or pinned host) ->
         updated x (device tensor owned by the engine)."""

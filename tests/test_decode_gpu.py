@@ -449,6 +449,12 @@ def test_engine_graph_capture_replays_identically():
     for _ in range(3):
         graphed = e.step(x0.cuda()).clone()
         assert torch.equal(eager, graphed)
+    # host in / host out in one graph launch (HybridDecodeRank.step_io)
+    x_host, y_host = x0.pin_memory(), torch.empty_like(x0).pin_memory()
+    for _ in range(2):
+        e.step_io(x_host, y_host)
+        torch.cuda.synchronize()
+        assert torch.equal(y_host, eager.cpu())
 
 
 @pytest.mark.parametrize("qpk", [4, 8])
