@@ -2,7 +2,8 @@
 //     out[n, c] (+)= sum_k x[n, k] * W[k, c]        n < 64 (the decode batch)
 // computed as D^T[128 cols x 64 rows] = W^T-tile . x^T with tcgen05.mma
 // (M = 128 weight columns, N = 64 batch rows, K = 16 per instruction; A = the
-// W tile, MN-major, B = x, K-major 128B-swizzled; fp32 accumulators in TMEM).
+// W^T tile, K-major when packed (MN-major when TMA-loaded from a row-major
+// W), B = x, K-major; both 128B-swizzled; fp32 accumulators in TMEM).
 //
 // Work decomposition: data-parallel split-K.  A CTA owns one column GROUP
 // (G = 1 or 2 adjacent 128-column tiles) and one of S equal k-ranges of it;
@@ -17,18 +18,21 @@
 //
 // The S splits of a group are one thread-block cluster.  Each CTA puts its
 // fp32 partial tile in its own shared memory; after a cluster barrier every
-// CTA sums its 1/S slice of the rows over all S tiles through distributed
-// shared memory, in split order (deterministic), and applies the epilogue;
-// a second barrier keeps the tiles alive for their readers.  No workspace,
-// no semaphores, no reduction launch.  S <= 8 is the largest split count
-// whose clusters are all co-resident (cudaOccupancyMaxActiveClusters).
+// CTA pushes row slice k of its tile to CTA k with one bulk copy into
+// distributed shared memory, and CTA k sums its slice over the S tiles in
+// split order (deterministic) and applies the epilogue; a closing barrier
+// keeps the source tiles alive until the copies landed.  No workspace, no
+// semaphores, no reduction launch.  S <= 8 is the largest split count whose
+// clusters are all co-resident (cudaOccupancyMaxActiveClusters).
 //
 // Roles (192 threads): warp 4 = TMA producer, warp 5 = MMA issuer, warps 0-3
-// = epilogue (TMEM lane quadrant = warp index).  Fused epilogues: plain
-// store, residual add (x += ...), and SwiGLU (tile = 64 gate + 64 up
-// columns -> 64 activations).  Launched with programmatic dependent launch:
-// the first W stages are fetched before griddepcontrol.wait, so the weight
-// stream starts while the previous kernel drains.
+// = epilogue (TMEM lane quadrant = warp index; idle during the main loop,
+// they run the epilogue code once with every side effect off, so its
+// instructions are cached when needed).  Fused epilogues: plain store,
+// residual add (x += ...), and SwiGLU (tile = 64 gate + 64 up columns -> 64
+// activations).  Launched with programmatic dependent launch: the first W
+// stages are fetched before griddepcontrol.wait, so the weight stream
+// starts while the previous kernel drains.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
