@@ -51,6 +51,7 @@ struct DecodeParams {
     int64_t n_warps;  // W of the stream-K partition
     int32_t tab_cache;  // decode_cta_kernel: page_off / item_seq staged in smem (n_items <= kTabItems)
     int32_t early;      // FS_DECODE_EARLY_PREFETCH: tables + first pages read before griddepcontrol.wait
+    int32_t l2_pf;      // (early) pages per warp past the ring prefetched into L2 before the wait
 };
 
 // items whose page offsets and block-table rows decode_cta_kernel stages in
@@ -618,6 +619,16 @@ extern "C" int fs_decode_attention(const fs_decode_desc *d, void *stream) {
     prm.part_lse = d->part_lse;
     prm.n_warps = W;
     prm.early = (d->flags & FS_DECODE_EARLY_PREFETCH) ? 1 : 0;
+    // (early) each warp also sends its 2 pages past the ring to L2 before
+    // griddepcontrol.wait, while the QKV GEMM leaves HBM under-used: C3 N=8
+    // rank step -1.8%, N=5 -0.9%, C2 -0.4%; 6+ pages, or a standing L2
+    // prefetch distance ahead of the ring, are slower
+    // (profiles/r02_k1_experiments/README.md).  FS_K1_L2_PREFETCH overrides.
+    static const int l2_pf = [] {
+        const char *e = getenv("FS_K1_L2_PREFETCH");
+        return e ? std::max(0, std::min(28, atoi(e))) : 2;
+    }();
+    prm.l2_pf = prm.early ? l2_pf : 0;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (d->config) {
 #define FS_CFG_CASE(i, w, s, c, k) \

@@ -107,6 +107,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_cta_kernel(const DecodeP
         ++px;
     };
     for (int s = 0; s < STAGES && px < n_my; ++s) issue(s);
+    if (lane >= STAGES && lane < STAGES + p.l2_pf && lane < n_my)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.kv + cur_pg * kPageBytes),
+                     "r"(kPageBytes) : "memory");
     grid_dependency_wait();  // q / kv_new come from the preceding GEMM
 
     // ---- consumer: items of the CTA range in order ----

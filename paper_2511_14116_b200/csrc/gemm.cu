@@ -81,6 +81,7 @@ struct GemmParams {
     float *ws;          // partial slots, each [64][128] fp32, slot = cta * G + g
     int32_t *sems;      // per group: arrive, depart (self-resetting)
     unsigned long long *dbg;  // optional per-CTA phase timestamps (ns)
+    int32_t l2_pf;      // packed W: stages past the prefetched ones sent to L2 before the wait
 };
 
 // ---------------------------------------------------------------- PTX ----
@@ -474,6 +475,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     // x comes from the preceding kernel: PDL wait, then the
                     // x halves of every stage issued so far
                     if (p.dbg) p.dbg[blockIdx.x * 16 + 5] = gtimer();
+                    if (p.w_packed && p.l2_pf > 0 && st + 1 < n_st) {
+                        const int b = k0 + (st + 1) * sps, e = min(k1, b + p.l2_pf * sps);
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                                     ::"l"(p.w_raw + ((int64_t)grp * p.nk + b) * G * kBlockW),
+                                     "r"((uint32_t)((e - b) * G * kBlockW)) : "memory");
+                    }
                     grid_dependency_wait();
                     waited = true;
                     if (p.dbg) p.dbg[blockIdx.x * 16 + 6] = gtimer();
@@ -807,6 +814,15 @@ extern "C" int fs_gemm_skinny(const void *x, int64_t ld_x, int32_t rows, int32_t
     prm.w_packed = w_layout != 0;
     prm.w_raw = static_cast<const uint8_t *>(w);
     prm.dbg = g_gemm_dbg;
+    // a CTA that starts under PDL before the previous kernel ends also sends
+    // its next 4 W stages to L2 (HBM is under-used in that window): C3 N=8
+    // rank step -0.5%, C2 -0.4%; 8 stages is slower at N=5
+    // (profiles/r02s4_gemm_notes.md).  FS_GEMM_L2_PREFETCH overrides.
+    static const int l2_pf = [] {
+        const char *e = getenv("FS_GEMM_L2_PREFETCH");
+        return e ? std::max(0, std::min(16, atoi(e))) : 4;
+    }();
+    prm.l2_pf = l2_pf;
     prm.out = static_cast<__nv_bfloat16 *>(out);
     prm.ld_out = ld_out;
     prm.res = static_cast<const __nv_bfloat16 *>(res);
