@@ -460,8 +460,8 @@ def test_engine_graph_capture_replays_identically():
 @pytest.mark.parametrize("qpk", [4, 8])
 def test_decode_long_context_per_item_tolerance(qpk):
     """The tolerance holds per long item, not only diluted over a launch:
-    bf16 P alone gives ~1.5e-3 mean-rel at 4k context; the kernels use f16
-    P against the f16 V pages."""
+    bf16 P alone gives ~1.5e-3 mean-rel at 4k context; the kernels use a
+    bf16 hi + lo pair of P against the bf16 V pages."""
     from oracle.attention import head_decode
     from oracle.placement import owner_table
     owner = owner_table("hybrid", 1, 8, range(8))
