@@ -64,10 +64,24 @@ def main(layers=None):
         eng.step_io(xh, yh)
         torch.cuda.current_stream().synchronize()
     print(f"step_io + sync per step: {(time.perf_counter() - t0) * 1e3 / steps:.4f} ms")
-    g = eng._io[0]
+    done = torch.cuda.Event()
     t0 = time.perf_counter()
     for _ in range(steps):
-        g.replay()
+        eng.step_io(xh, yh)
+        done.record()
+        while not done.query():
+            pass
+    print(f"step_io + spin-wait per step: {(time.perf_counter() - t0) * 1e3 / steps:.4f} ms")
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        eng.step()
+        done.record()
+        while not done.query():
+            pass
+    print(f"replay + spin-wait per step: {(time.perf_counter() - t0) * 1e3 / steps:.4f} ms")
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        eng._io[0].replay()
     t1 = time.perf_counter()
     torch.cuda.synchronize()
     print(f"step_io graph launch CPU cost: {(t1 - t0) * 1e6 / steps:.1f} us")
