@@ -234,12 +234,13 @@ def test_c2_full_layer_vs_float64_layer(gemm):
     torch.cuda.empty_cache()
 
 
-def test_c3_n5_full_layer_vs_float64_layer():
+@pytest.mark.parametrize("fails", [(), (7,), (7, 3), (7, 3, 5)])
+def test_c3_full_layer_vs_float64_layer(fails):
     """One whole C3-shaped decode layer (hidden 8192, 64q / 8kv, FFN 28672,
-    B=64; context 1024 to keep the float64 cache small) on the N=5
-    on-demand target (8 -> 7 -> 6 -> 5 after GPUs 7, 3, 5 fail: 1 TP + 3 DP
-    heads per rank, FFN shards 45/45/45/45/44), through the five ranks'
-    engines (``emulated_parallel_step``: each rank's QKV GEMM + K1 + O
+    B=64; context 1024 to keep the float64 cache small) on hybrid(8) and on
+    the on-demand targets of 7 / 6 / 5 survivors (GPUs 7, 3, 5 fail: 1 TP
+    + 1 / 2 / 3 DP heads per rank; at N=5 FFN shards 45/45/45/45/44),
+    through every rank's engine (``emulated_parallel_step``: each rank's QKV GEMM + K1 + O
     partial, ordered fp32 sum over ranks, residual; then each rank's gated
     MLP partial over its shards, sum, residual) against
     ``oracle.decode_step.DecodeLayerF64`` running the WHOLE layer on one
@@ -256,7 +257,7 @@ def test_c3_n5_full_layer_vs_float64_layer():
     B, ctx, hd, qpk, H, hid = 64, 1024, 128, 8, 8, 8192
     model = _model(1, hid, 64, 28672)
     plan, alive = make_placement("hybrid", model, range(8)), list(range(8))
-    for f in (7, 3, 5):
+    for f in fails:
         alive = [g for g in alive if g != f]
         plan = plan_weight_recovery(model, plan, alive, "on_demand").target_plan("hybrid", model)
     owner = owner_array(plan, H)
@@ -305,10 +306,11 @@ def test_c3_n5_full_layer_vs_float64_layer():
         ref = lay.step(xd, ctx - 1, pool)
     upd = np.abs(ref - xd).mean()
     err = np.abs(got - ref)
-    print(f"C3 N=5 layer: max-abs {err.max():.3e} mean-abs {err.mean():.3e} "
+    print(f"C3 N={len(alive)} layer: max-abs {err.max():.3e} mean-abs {err.mean():.3e} "
           f"mean |update| {upd:.3e} mean |x| {np.abs(ref).mean():.3e}")
-    # measured on a B200: max-abs 2.2e-2, mean-abs 1.93e-3 against a mean
-    # |update| of 0.238 (bounds as in the C2 whole-layer test)
+    # measured on a B200, N = 8 / 7 / 6 / 5: max-abs 2.2e-2 / 3.1e-2 / 2.2e-2 /
+    # 2.2e-2, mean-abs 1.93e-3 each, against a mean |update| of 0.238
+    # (bounds as in the C2 whole-layer test)
     assert err.max() <= 4e-2, (err.max(), upd)
     assert err.mean() <= 1.5e-2 * upd, (err.mean(), upd)
     assert np.abs(got - xd).mean() > 0.1 * upd
