@@ -85,6 +85,57 @@ class DecodeLayerF64:
         return x + (_silu(hgu[:, :C]) * hgu[:, C:]) @ self.wd  # refexec.py:299-307
 
 
+class MixedIterationF64:
+    """Float64 restatement of one serving iteration over all layers
+    (TEST INFRASTRUCTURE): the token rows of a mixed batch -- prefill-chunk
+    tokens and decode tokens, each a (request, position) pair
+    (simulation.py:413-443) -- are projected to q/k/v (refexec.py:88-90),
+    every row's K/V joins its request's cache at its position, and every row
+    attends its request's positions 0..pos, causal including itself (the
+    multi-row ``rows`` mask of ``_head_attention``, refexec.py:91-101), with
+    q-head j reading KV head j // qpk (core.py:71-72); then the output
+    projection and residual (refexec.py:298) and the gated MLP and residual
+    (refexec.py:299-307).  The cache persists across calls, as the
+    iterations of a trace do.
+
+    ``layers``: per layer (wqkv [hidden, (H*qpk + 2H)*hd] as [q heads | k
+    heads | v heads], wo [H*qpk*hd, hidden], wgu [hidden, 2C] as [gate | up],
+    wd [C, hidden]), float64."""
+
+    def __init__(self, H, qpk, hd, layers):
+        self.H, self.qpk, self.hd, self.layers = H, qpk, hd, layers
+        self.kv = {}  # (layer, head, request) -> {position: (k, v)}
+
+    def step(self, rows, x):
+        H, qpk, hd = self.H, self.qpk, self.hd
+        qw = H * qpk * hd
+        scale = 1.0 / np.sqrt(hd)
+        for layer, (wqkv, wo, wgu, wd) in enumerate(self.layers):
+            qkv = x @ wqkv
+            for t, (r, pos) in enumerate(rows):
+                for h in range(H):
+                    self.kv.setdefault((layer, h, r), {})[pos] = (
+                        qkv[t, qw + h * hd:qw + (h + 1) * hd],
+                        qkv[t, qw + (H + h) * hd:qw + (H + h + 1) * hd])
+            o = np.zeros((len(rows), qw))
+            for t, (r, pos) in enumerate(rows):
+                for h in range(H):
+                    cache = self.kv[(layer, h, r)]
+                    k = np.stack([cache[p][0] for p in range(pos + 1)])
+                    v = np.stack([cache[p][1] for p in range(pos + 1)])
+                    q = qkv[t, h * qpk * hd:(h + 1) * qpk * hd].reshape(qpk, hd)
+                    s = (q @ k.T) * scale
+                    s -= s.max(axis=1, keepdims=True)
+                    w = np.exp(s)
+                    w /= w.sum(axis=1, keepdims=True)
+                    o[t, h * qpk * hd:(h + 1) * qpk * hd] = (w @ v).reshape(-1)
+            x = x + o @ wo
+            hgu = x @ wgu
+            C = hgu.shape[1] // 2
+            x = x + (_silu(hgu[:, :C]) * hgu[:, C:]) @ wd
+        return x
+
+
 class _one_blas_thread:
     def __enter__(self):
         try:

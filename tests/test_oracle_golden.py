@@ -204,3 +204,34 @@ def test_prefill_restatement(golden):
             np.testing.assert_allclose(out, np.array(c["out"][k:k + cn]), rtol=0, atol=1e-12)
             start += length
             k += cn
+
+
+def test_mixed_iteration_oracle_matches_decode_oracle():
+    """oracle.decode_step.MixedIterationF64 on a decode-only batch equals
+    DecodeLayerF64 (itself checked against the golden decode rows via
+    oracle.attention) on the same weights and history; on a prefill chunk
+    its rows equal a token-by-token decode of the same tokens."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle.decode_step import DecodeLayerF64, MixedIterationF64
+    H, qpk, hd, B, ctx = 2, 2, 16, 3, 6
+    lay = DecodeLayerF64(32, H, qpk, hd, 24, B, ctx, seed=3)
+    ws = [(lay.wqkv, lay.wo, lay.wgu, lay.wd)]
+    mix = MixedIterationF64(H, qpk, hd, ws)
+    pos = ctx - 1
+    for h in range(H):
+        for r in range(B):
+            mix.kv[(0, h, r)] = {p: (lay.k[h, r, p].copy(), lay.v[h, r, p].copy())
+                                 for p in range(pos)}
+    x = np.random.default_rng(4).standard_normal((B, 32))
+    got = mix.step([(r, pos) for r in range(B)], x)
+    with ThreadPoolExecutor(2) as pool:
+        ref = lay.step(x.copy(), pos, pool)
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
+    # a 3-token prefill chunk of request 0 == three decode steps of it
+    chunk = MixedIterationF64(H, qpk, hd, ws)
+    seq = MixedIterationF64(H, qpk, hd, ws)
+    xc = np.random.default_rng(5).standard_normal((3, 32))
+    a = chunk.step([(0, 0), (0, 1), (0, 2)], xc)
+    b = np.concatenate([seq.step([(0, p)], xc[p:p + 1]) for p in range(3)])
+    np.testing.assert_allclose(a, b, rtol=1e-12, atol=1e-12)

@@ -132,6 +132,42 @@ def test_serving_matches_dense_reference(qpk):
         _close(g, r)
 
 
+@pytest.mark.parametrize("qpk", [4, 8])
+def test_serving_matches_float64_oracle(qpk):
+    """The same mixed prefill/decode iterations against the float64 oracle
+    (``oracle.decode_step.MixedIterationF64``) on the engine's bf16 weights
+    and inputs: the engine rounds qkv, attention output, x and the MLP
+    activation to bf16 and the oracle carries float64, so the bound is on
+    each iteration's output relative to the scale of its update."""
+    from oracle.decode_step import MixedIterationF64
+    from paper_2511_14116_b200.placement import make_placement, owner_array
+    model = _model(qpk)
+    inputs = [(40, 5), (17, 3), (100, 4), (3, 6), (64, 2)]
+    routing, steps, caps = _iterations(model, [0], inputs, budget=48, n_iter=6)
+    plan = make_placement("hybrid", model, [0])
+    owner = owner_array(plan, 8)
+    shards = [plan.ffn.owner[s] for s in range(plan.ffn.num_shards)]
+    eng = _engine(model, owner, 0, routing, caps, shards, 64)
+    assert list(eng.work.slot_heads[0]) == list(range(8))  # slot j is head j at world 1
+    f64 = (lambda t: t.double().cpu().numpy())
+    ora = MixedIterationF64(8, qpk, 128, [(f64(eng.wqkv[l]), f64(eng.wo[l]), f64(eng.w_gu[l]),
+                                          f64(eng.w_d[l])) for l in range(model.num_layers)])
+    gen = torch.Generator().manual_seed(7)
+    worst = 0.0
+    for s in steps:
+        x = torch.randn((s.num_tokens, 512), generator=gen).to(torch.bfloat16)
+        got = f64(eng.serve(eng.plan(s), x.cuda()))
+        rows = [(r, p0 + j) for r, p0, n in s.prefill for j in range(n)] + list(s.decode)
+        xd = f64(x)
+        ref = ora.step(rows, xd)
+        upd = np.abs(ref - xd).mean()
+        err = np.abs(got - ref)
+        assert err.max() <= 4e-2, (err.max(), upd)
+        assert err.mean() <= 2e-2 * upd, (err.mean(), upd)
+        worst = max(worst, err.mean() / upd)
+    print(f"serving vs float64 (qpk {qpk}): worst mean-abs / mean |update| {worst:.3e}")
+
+
 @pytest.mark.parametrize("world,fail", [(3, None), (8, 7), (6, None)])
 def test_serving_partition_matches_single_rank(world, fail):
     """Hybrid partition (and the on-demand target after losing GPU 7 of 8):
