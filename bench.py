@@ -10,12 +10,13 @@ N ranks (hybrid placement, least-loaded routing, NCCL all-reduce of the
 attention output).  One JSON line on rank 0.
 
 A *step* = one decode token for all 64 requests through every layer:
-fused QKV GEMM (cuBLAS) -> ONE fs_decode_attention launch (KV append + paged
-GQA decode + split merge) -> output projection -> exchange + residual (N>1:
-one fs_ar_residual kernel over IPC-mapped peer buffers, ``--exchange nccl``
-for an NCCL all-reduce) -> TP MLP partial over the rank's FFN shards (gate/up
-GEMM, fs_swiglu, down GEMM) -> exchange -> residual (``--no-mlp``: attention
-sublayer only).  The whole step is one CUDA-graph replay.  The KV working set
+fused QKV GEMM (fs_gemm_skinny, tcgen05; ``--gemm cublas`` for cuBLAS) -> ONE
+fs_decode_attention launch (KV append + paged GQA decode + split merge) ->
+output projection (+ residual at N=1) -> exchange + residual (N>1: one
+fs_ar_residual kernel over IPC-mapped peer buffers, ``--exchange nccl`` for an
+NCCL all-reduce) -> TP MLP partial over the rank's FFN shards (gate/up GEMM
+with the SwiGLU epilogue, down GEMM) -> exchange -> residual (``--no-mlp``:
+attention sublayer only).  The whole step is one CUDA-graph replay.  The KV working set
 (34 GB at N=1) is far larger than L2, so no flush is needed between steps.
 
 At N=1 the line also carries (rank 0 only):
@@ -664,7 +665,8 @@ def workload_config(world, batch=64, ctx=4096):
     c = C2_SHAPE
     return {"workload": "C2 Llama-3-8B-shaped hybrid-attention decode step, all 32 layers: "
                         "QKV GEMM, fused KV-append + paged GQA decode, O GEMM, TP MLP "
-                        "partial (gate/up GEMM, swiglu, down GEMM); when N>1 the attention and MLP "
+                        "partial (gate/up GEMM with fused SwiGLU, down GEMM); when N>1 the "
+                        "attention and MLP "
                         "partials are exchanged by fs_ar_residual (ordered sum + residual in one "
                         "kernel over IPC-mapped peer buffers; --exchange nccl: NCCL all-reduce)",
             "layers": c["layers"], "q_heads": c["kv_heads"] * c["qpk"],
